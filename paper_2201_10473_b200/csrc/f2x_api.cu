@@ -1,0 +1,414 @@
+// Host side of the engine: planner, the C ABI of include/f2x.h, and the
+// three memory-side kernels around the node kernel (f2x_kernels.cuh):
+//   K1 k1_slice      packed uint64[batch][t] -> bitsliced chunked groups
+//                    (+ constant-time top-bit check for ring operands)
+//   K2 k2_node_mul   per (group, Karatsuba path) node product  [hot kernel]
+//   K3 k3_interp<D>  global Karatsuba interpolation, D levels per pass
+//   K4 k4_unslice    fold mod X^n-1 (cyclic) + transpose back to uint64 rows
+// Reference interfaces replaced: schoolbook_mul (poly.py:547-561),
+// clmul64_batch (poly.py:451-480), SPEC ring_mul.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/f2x.h"
+#include "f2x_kernels.cuh"
+
+namespace f2x {
+
+extern const K2Entry k2_part0[];
+extern const int k2_part0_n;
+extern const K2Entry k2_part1[];
+extern const int k2_part1_n;
+extern const K2Entry k2_part2[];
+extern const int k2_part2_n;
+extern const K2Entry k2_part3[];
+extern const int k2_part3_n;
+
+static const K2Entry *find_k2(int LF, int KC) {
+    const K2Entry *parts[4] = {k2_part0, k2_part1, k2_part2, k2_part3};
+    const int ns[4] = {k2_part0_n, k2_part1_n, k2_part2_n, k2_part3_n};
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < ns[i]; ++j)
+            if (parts[i][j].LF == LF && parts[i][j].KC == KC) return &parts[i][j];
+    return nullptr;
+}
+
+static constexpr int kMaxKC = 5;
+static constexpr int kMaxGL = 8;
+static constexpr int kMaxPassLevels = 3;
+static constexpr int kThreads = 128;
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+static inline int64_t ipow3(int k) {
+    int64_t r = 1;
+    while (k-- > 0) r *= 3;
+    return r;
+}
+
+// ------------------------------------------------------------------- K1
+// One thread = one (group, operand word u): 32 rows x 64 coefficients.
+__global__ void __launch_bounds__(kThreads)
+k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
+         uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
+         int ncyc, uint32_t *d_err, int UB, int64_t items) {
+    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item >= items) return;
+    const int64_t g = item / UB;
+    const int u = int(item - g * UB);
+    const uint64_t *X = blockIdx.y ? B : A;
+    uint32_t *out = (blockIdx.y ? Bbs : Abs) + g * Ns;
+
+    uint32_t lo[32], hi[32];
+    uint64_t bad = 0;
+    const uint64_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u < 64)
+                                ? (~0ull << (ncyc - 64 * u)) : 0ull;
+#pragma unroll
+    for (int pr = 0; pr < 32; ++pr) {
+        const int64_t row = g * 32 + pr;
+        const uint64_t v = (row < batch && u < t) ? __ldg(X + row * t + u) : 0ull;
+        bad |= v & himask;
+        lo[pr] = uint32_t(v);
+        hi[pr] = uint32_t(v >> 32);
+    }
+    if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
+        atomicOr(d_err, uint32_t((bad | (bad >> 32)) != 0));
+    transpose32(lo);
+    transpose32(hi);
+
+    // coefficient k = 64u + i -> storage (k / LF) * LFS + k % LF
+    const int k0 = 64 * u;
+    int c = k0 / LF, r = k0 - c * LF;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        if (k0 + i < N) out[int64_t(c) * LFS + r] = i < 32 ? lo[i] : hi[i - 32];
+        if (++r == LF) {
+            r = 0;
+            ++c;
+        }
+    }
+    // zero the pad words of every chunk that starts inside [k0, k0 + 64)
+    if (LFS > LF) {
+        for (int cc = (k0 + LF - 1) / LF; cc * LF < min(k0 + 64, N); ++cc)
+            for (int rr = LF; rr < LFS; ++rr) out[int64_t(cc) * LFS + rr] = 0u;
+    }
+}
+
+// ------------------------------------------------------------------- K3
+// Global Karatsuba interpolation, D levels in one pass.  Node products are
+// split into 4 quarters; a node's quarter index w only touches its
+// children's quarter index w, so each thread owns one w of one top node and
+// rebuilds the D-level subtree in registers.
+template <int D>
+__device__ __forceinline__ void k3_rec(uint32_t *out, const uint32_t *__restrict__ Pin,
+                                       int64_t inStride, int64_t desc, int qw, int w) {
+    if constexpr (D == 0) {
+        const uint32_t *src = Pin + desc * inStride + w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = __ldg(src + int64_t(q) * qw);
+    } else {
+        constexpr int Lc = 2 << D;  // child vector length
+        constexpr int half = Lc / 2;
+        k3_rec<D - 1>(out, Pin, inStride, desc * 3 + 0, qw, w);
+        k3_rec<D - 1>(out + Lc, Pin, inStride, desc * 3 + 1, qw, w);
+        uint32_t m[Lc];
+        k3_rec<D - 1>(m, Pin, inStride, desc * 3 + 2, qw, w);
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const uint32_t T = out[half + i] ^ out[Lc + i];
+            out[half + i] = T ^ out[i] ^ m[i];
+            out[Lc + i] = T ^ out[Lc + half + i] ^ m[half + i];
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t items, int qw,
+          int64_t inStride, int64_t outStride) {
+    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item >= items) return;
+    const int64_t node = item / qw;
+    const int w = int(item - node * qw);
+    uint32_t v[4 << D];
+    k3_rec<D>(v, Pin, inStride, node * pow3c(D), qw, w);
+    uint32_t *dst = Pout + node * outStride + w;
+#pragma unroll
+    for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qw] = v[m];
+}
+
+// ------------------------------------------------------------------- K4
+// One thread = one (group, output word u): fold (cyclic), transpose, store.
+__global__ void __launch_bounds__(kThreads)
+k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
+           int LF, int LFS, int64_t rootStride, int ncyc, int64_t items) {
+    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item >= items) return;
+    const int64_t g = item / tout;
+    const int u = int(item - g * tout);
+    const uint32_t *Cg = Croot + g * rootStride;
+
+    uint32_t lo[32], hi[32];
+    const int k0 = 64 * u;
+    int c = k0 / LF, r = k0 - c * LF;
+    if (ncyc > 0) {
+        const int k1 = k0 + ncyc;
+        int c2 = k1 / LF, r2 = k1 - c2 * LF;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            uint32_t v = 0u;
+            if (k0 + i < ncyc) v = __ldg(Cg + int64_t(c) * LFS + r) ^ __ldg(Cg + int64_t(c2) * LFS + r2);
+            if (i < 32) lo[i] = v; else hi[i - 32] = v;
+            if (++r == LF) { r = 0; ++c; }
+            if (++r2 == LF) { r2 = 0; ++c2; }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const uint32_t v = __ldg(Cg + int64_t(c) * LFS + r);
+            if (i < 32) lo[i] = v; else hi[i - 32] = v;
+            if (++r == LF) { r = 0; ++c; }
+        }
+    }
+    transpose32(lo);
+    transpose32(hi);
+#pragma unroll
+    for (int pr = 0; pr < 32; ++pr) {
+        const int64_t row = g * 32 + pr;
+        if (row < batch) out[row * tout + u] = uint64_t(lo[pr]) | (uint64_t(hi[pr]) << 32);
+    }
+}
+
+// ---------------------------------------------------------------- planner
+struct Layout {
+    int64_t Ns, Ss;
+    int64_t off_abs, off_bbs, off_p0, off_p1, total;
+};
+
+static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
+                     Layout *lay) {
+    if (!pl || batch < 1 || t_or_n < 1) return F2X_EINVAL;
+    std::memset(pl, 0, sizeof(*pl));
+    int t, n;
+    if (kind == F2X_KIND_FULL) {
+        t = t_or_n;
+        if (t > (1 << 20)) return F2X_ERANGE;
+        n = 64 * t;
+    } else if (kind == F2X_KIND_CYCLIC) {
+        n = t_or_n;
+        t = (n + 63) / 64;
+    } else {
+        return F2X_EINVAL;
+    }
+    const int64_t Nmin = int64_t(64) * t;
+    int bestLF = 0, bestK = 0;
+    double best = 0;
+    for (int K = 1; K <= kMaxKC + kMaxGL; ++K) {
+        int64_t LF = ceil_div(Nmin, int64_t(1) << K);
+        if (K >= kMaxKC) {
+            if (LF < 16) LF = 16;
+            if (LF > 40) continue;
+        } else {
+            LF = LF <= 16 ? 16 : (LF <= 32 ? 32 : 0);
+            if (!LF) continue;
+        }
+        if (leaf_hint) {
+            if (LF > leaf_hint) continue;
+            LF = leaf_hint;
+        }
+        const int KC = std::min(K, kMaxKC);
+        if (!find_k2(int(LF), KC)) continue;
+        const double cost = double(ipow3(K)) * double(LF * LF + 16 * LF);
+        if (!bestLF || cost < best) {
+            best = cost;
+            bestLF = int(LF);
+            bestK = K;
+        }
+        if (leaf_hint) break;  // smallest K that fits the forced leaf
+    }
+    if (!bestLF) return F2X_ERANGE;
+    const int LF = bestLF, K = bestK, KC = std::min(K, kMaxKC), GL = K - KC;
+    const K2Entry *e = find_k2(LF, KC);
+    const int LFS = (LF + 3) & ~3;
+
+    pl->kind = kind;
+    pl->t = t;
+    pl->n = n;
+    pl->N = LF << K;
+    pl->batch = batch;
+    pl->groups = ceil_div(batch, 32);
+    pl->leaf_words = LF;
+    pl->leaf_stride = LFS;
+    pl->levels = K;
+    pl->cta_levels = KC;
+    pl->global_levels = GL;
+    int rem = GL, np = 0;
+    while (rem > 0) {
+        const int p = std::min(kMaxPassLevels, rem);
+        pl->pass_levels[np++] = p;
+        rem -= p;
+    }
+    pl->num_passes = np;
+    pl->launches = 3 + np;
+    pl->cta_threads = e->threads;
+    pl->node_ctas = pl->groups * ipow3(GL);
+    pl->node_smem_bytes = int64_t(e->smem);
+    // analytic operation counts per product (bitsliced: 1 LOP3 = 32 products)
+    pl->leaf_ops_per_product = double(ipow3(K)) * LF * LF / 32.0;
+    {
+        // eval: each level-j node writes one mid of h_j words per operand;
+        // interp: 3 XOR-ops per half word.  Summed over all K levels.
+        double ev = 0, ip = 0;
+        for (int j = 0; j < K; ++j) {
+            const double hj = double(int64_t(LF) << (K - j - 1));
+            ev += 2.0 * double(ipow3(j)) * hj;
+            ip += 3.0 * double(ipow3(j)) * hj;
+        }
+        pl->karatsuba_ops_per_product = (ev + ip) / 32.0;
+    }
+    Layout L;
+    L.Ns = int64_t(LFS) << K;
+    L.Ss = int64_t(LFS) << KC;
+    const int64_t G = pl->groups;
+    L.off_abs = 0;
+    L.off_bbs = align256(L.off_abs + G * L.Ns * 4);
+    L.off_p0 = align256(L.off_bbs + G * L.Ns * 4);
+    const int64_t p0 = G * ipow3(GL) * 2 * L.Ss * 4;
+    L.off_p1 = align256(L.off_p0 + p0);
+    int64_t p1 = 0;
+    if (np >= 2) {
+        const int d1 = GL - pl->pass_levels[0];
+        p1 = G * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
+    }
+    L.total = align256(L.off_p1 + p1);
+    pl->workspace_bytes = L.total;
+    if (lay) *lay = L;
+    return F2X_OK;
+}
+
+template <int D>
+static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw, int64_t inS,
+                     int64_t outS, cudaStream_t s) {
+    k3_interp<D><<<unsigned(ceil_div(items, kThreads)), kThreads, 0, s>>>(Pin, Pout, items, qw,
+                                                                            inS, outS);
+    return 0;
+}
+
+static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int64_t batch,
+               int t_or_n, void *ws, size_t ws_bytes, int leaf_hint, uint32_t *d_err,
+               cudaStream_t stream) {
+    if (!A || !B || !C || !ws) return F2X_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+         reinterpret_cast<uintptr_t>(C) | reinterpret_cast<uintptr_t>(ws)) & 15)
+        return F2X_EINVAL;
+    f2x_plan pl;
+    Layout L;
+    int rc = plan_impl(kind, batch, t_or_n, leaf_hint, &pl, &L);
+    if (rc) return rc;
+    if (int64_t(ws_bytes) < L.total) return F2X_ENOSPC;
+    char *w = static_cast<char *>(ws);
+    uint32_t *Abs = reinterpret_cast<uint32_t *>(w + L.off_abs);
+    uint32_t *Bbs = reinterpret_cast<uint32_t *>(w + L.off_bbs);
+    uint32_t *P0 = reinterpret_cast<uint32_t *>(w + L.off_p0);
+    uint32_t *P1 = reinterpret_cast<uint32_t *>(w + L.off_p1);
+    const int64_t G = pl.groups;
+    const int ncyc = kind == F2X_KIND_CYCLIC ? pl.n : 0;
+
+    // K1
+    const int UB = int(ceil_div(pl.N, 64));
+    {
+        const int64_t items = G * UB;
+        dim3 grid(unsigned(ceil_div(items, kThreads)), 2);
+        k1_slice<<<grid, kThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N, pl.leaf_words,
+                                                pl.leaf_stride, L.Ns, ncyc, d_err, UB, items);
+    }
+    // K2
+    const K2Entry *e = find_k2(pl.leaf_words, pl.cta_levels);
+    K2Params kp;
+    kp.Abs = Abs;
+    kp.Bbs = Bbs;
+    kp.Pout = P0;
+    kp.Ns = L.Ns;
+    kp.K = pl.levels;
+    kp.GL = pl.global_levels;
+    kp.paths = int(ipow3(pl.global_levels));
+    rc = e->launch(kp, pl.node_ctas, stream);
+    if (rc) return rc;
+    // K3 passes
+    uint32_t *cur = P0, *nxt = P1;
+    int d = pl.global_levels;
+    for (int i = 0; i < pl.num_passes; ++i) {
+        const int D = pl.pass_levels[i];
+        const int dlo = d - D;
+        const int64_t Shi = L.Ns >> d, Slo = L.Ns >> dlo;
+        const int qw = int(Shi / 2);
+        const int64_t items = G * ipow3(dlo) * qw;
+        switch (D) {
+            case 1: launch_k3<1>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
+            case 2: launch_k3<2>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
+            case 3: launch_k3<3>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
+            default: return F2X_ERANGE;
+        }
+        std::swap(cur, nxt);
+        d = dlo;
+    }
+    // K4
+    {
+        const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
+        const int64_t items = G * tout;
+        k4_unslice<<<unsigned(ceil_div(items, kThreads)), kThreads, 0, stream>>>(
+            cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, items);
+    }
+    const cudaError_t ce = cudaGetLastError();
+    return ce == cudaSuccess ? F2X_OK : F2X_ECUDA - int(ce);
+}
+
+}  // namespace f2x
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int f2x_make_plan(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint,
+                  f2x_plan *plan) {
+    return f2x::plan_impl(kind, batch, t_or_n, leaf_hint, plan, nullptr);
+}
+
+int64_t f2x_workspace_bytes(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint) {
+    f2x_plan pl;
+    const int rc = f2x::plan_impl(kind, batch, t_or_n, leaf_hint, &pl, nullptr);
+    return rc ? rc : pl.workspace_bytes;
+}
+
+int f2x_mul_full(const uint64_t *A, const uint64_t *B, uint64_t *C, int64_t batch, int32_t t,
+                 void *workspace, size_t workspace_bytes, int32_t leaf_hint, void *stream) {
+    return f2x::run(F2X_KIND_FULL, A, B, C, batch, t, workspace, workspace_bytes, leaf_hint,
+                    nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int f2x_mul_cyclic(const uint64_t *A, const uint64_t *B, uint64_t *C, int64_t batch, int32_t n,
+                   void *workspace, size_t workspace_bytes, int32_t leaf_hint, uint32_t *d_err,
+                   void *stream) {
+    return f2x::run(F2X_KIND_CYCLIC, A, B, C, batch, n, workspace, workspace_bytes, leaf_hint,
+                    d_err, static_cast<cudaStream_t>(stream));
+}
+
+int f2x_clmul64(const uint64_t *a, const uint64_t *b, uint64_t *lohi, int64_t lanes,
+                void *workspace, size_t workspace_bytes, void *stream) {
+    return f2x::run(F2X_KIND_FULL, a, b, lohi, lanes, 1, workspace, workspace_bytes, 0, nullptr,
+                    static_cast<cudaStream_t>(stream));
+}
+
+const char *f2x_strerror(int code) {
+    if (code == F2X_OK) return "ok";
+    if (code == F2X_EINVAL) return "invalid argument (batch/t/n < 1, null or misaligned pointer)";
+    if (code == F2X_ENOSPC) return "workspace too small (see f2x_workspace_bytes)";
+    if (code == F2X_ERANGE) return "operand size outside the supported envelope";
+    if (code <= F2X_ECUDA) return cudaGetErrorString(static_cast<cudaError_t>(F2X_ECUDA - code));
+    return "unknown error";
+}
+
+int f2x_version(void) { return 100; }
+
+}  // extern "C"

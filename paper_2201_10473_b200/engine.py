@@ -1,0 +1,136 @@
+"""Batched device API over the C ABI (torch CUDA tensors in, tensors out).
+
+``mul_full``   -- rows of ``schoolbook_mul`` (poly.py:547-561), [B,t] -> [B,2t]
+``mul_cyclic`` -- rows of the SPEC ``ring_mul``, [B,t] -> [B,t]
+
+Operands are ``torch.uint64`` (or the same bits viewed as ``torch.int64``)
+CUDA tensors in the reference's packed little-endian word layout
+(poly.py:4-8).  Work is enqueued on the current torch stream.  torch only
+provides device memory and streams here; all arithmetic is in libf2x.so.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _lib
+
+_WORDS = (torch.uint64, torch.int64)
+_ws_lock = threading.Lock()
+_workspaces: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def _workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> torch.Tensor:
+    """Grow-only scratch per (device, stream); allocated outside the hot loop
+    once the largest shape has been seen."""
+    key = (device.index, stream.cuda_stream)
+    with _ws_lock:
+        ws = _workspaces.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            _workspaces[key] = ws
+        return ws
+
+
+def _check_operands(A: torch.Tensor, B: torch.Tensor) -> None:
+    if not isinstance(A, torch.Tensor) or not isinstance(B, torch.Tensor):
+        raise TypeError("operands must be torch tensors")
+    if A.dtype not in _WORDS or B.dtype not in _WORDS:
+        raise ValueError("operands must be uint64 (or int64-viewed) word tensors")
+    if A.dim() != 2 or A.shape != B.shape:
+        raise ValueError(f"operands must be equal-shape [batch, t]; got {tuple(A.shape)} "
+                         f"and {tuple(B.shape)}")
+    if A.shape[1] < 1:
+        raise ValueError("zero-length polynomials are rejected; need t >= 1")
+    if not A.is_cuda or A.device != B.device:
+        raise ValueError("operands must live on the same CUDA device")
+    if not A.is_contiguous() or not B.is_contiguous():
+        raise ValueError("operands must be contiguous")
+
+
+def plan(kind: str, batch: int, t_or_n: int, leaf: int = 0) -> dict:
+    """The engine's plan for a call shape (see include/f2x.h ``f2x_plan``)."""
+    k = _lib.KIND_FULL if kind == "full" else _lib.KIND_CYCLIC
+    return _lib.make_plan(k, batch, t_or_n, leaf).as_dict()
+
+
+def mul_full(A: torch.Tensor, B: torch.Tensor, *, out: torch.Tensor | None = None,
+             leaf: int = 0) -> torch.Tensor:
+    """C[r] = A[r] * B[r] over F2[X] for every row r; C has 2t words."""
+    _check_operands(A, B)
+    batch, t = A.shape
+    if out is None:
+        out = torch.empty((batch, 2 * t), dtype=A.dtype, device=A.device)
+    elif out.shape != (batch, 2 * t) or out.dtype not in _WORDS or not out.is_contiguous() \
+            or out.device != A.device:
+        raise ValueError("out must be a contiguous [batch, 2t] word tensor on A's device")
+    if batch == 0:
+        return out
+    lib = _lib.load()
+    with torch.cuda.device(A.device):
+        stream = torch.cuda.current_stream(A.device)
+        need = lib.f2x_workspace_bytes(_lib.KIND_FULL, batch, t, leaf)
+        if need < 0:
+            _lib.check(int(need), "f2x_workspace_bytes")
+        ws = _workspace(A.device, stream, need)
+        rc = lib.f2x_mul_full(A.data_ptr(), B.data_ptr(), out.data_ptr(), batch, t,
+                              ws.data_ptr(), ws.numel(), leaf, stream.cuda_stream)
+    _lib.check(rc, "f2x_mul_full")
+    return out
+
+
+def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | None = None,
+               leaf: int = 0, check: bool = True,
+               err_flag: torch.Tensor | None = None) -> torch.Tensor:
+    """C[r] = A[r] * B[r] mod X^n - 1 for every row r (t = ceil(n/64) words).
+
+    Inputs with any bit >= n set are rejected with ValueError (SPEC.md:349,
+    369).  The check is fused into the first kernel as a constant-time
+    OR-reduction into a device flag; with ``check=True`` the call
+    synchronises and raises.  With ``check=False`` the caller passes
+    ``err_flag`` (a zeroed int32/uint32 CUDA tensor of one element) and
+    inspects it later -- the asynchronous form used inside timed loops.
+    """
+    _check_operands(A, B)
+    n = int(n)
+    if n < 1:
+        raise ValueError("ring degree n must be >= 1")
+    batch, t = A.shape
+    if t != (n + 63) // 64:
+        raise ValueError(f"ring operands need {(n + 63) // 64} words for n={n}, got {t}")
+    if out is None:
+        out = torch.empty((batch, t), dtype=A.dtype, device=A.device)
+    elif out.shape != (batch, t) or out.dtype not in _WORDS or not out.is_contiguous() \
+            or out.device != A.device:
+        raise ValueError("out must be a contiguous [batch, t] word tensor on A's device")
+    if batch == 0:
+        return out
+    lib = _lib.load()
+    with torch.cuda.device(A.device):
+        stream = torch.cuda.current_stream(A.device)
+        flag = err_flag
+        if flag is None:
+            flag = torch.zeros(1, dtype=torch.int32, device=A.device)
+        need = lib.f2x_workspace_bytes(_lib.KIND_CYCLIC, batch, n, leaf)
+        if need < 0:
+            _lib.check(int(need), "f2x_workspace_bytes")
+        ws = _workspace(A.device, stream, need)
+        rc = lib.f2x_mul_cyclic(A.data_ptr(), B.data_ptr(), out.data_ptr(), batch, n,
+                                ws.data_ptr(), ws.numel(), leaf, flag.data_ptr(),
+                                stream.cuda_stream)
+    _lib.check(rc, "f2x_mul_cyclic")
+    if check and err_flag is None and int(flag.item()) != 0:
+        raise ValueError("operand has bits set at or above n")
+    return out
+
+
+def clmul64_lanes(a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Lane-wise 64x64 -> 128 carry-less products (clmul64_batch), device tensors."""
+    if a.dim() != 1 or a.shape != b.shape:
+        raise ValueError("lane arrays must be equal-length 1-D")
+    if a.numel() == 0:
+        return a.clone(), a.clone()
+    lohi = mul_full(a.reshape(-1, 1).contiguous(), b.reshape(-1, 1).contiguous())
+    return lohi[:, 0], lohi[:, 1]

@@ -1,0 +1,239 @@
+"""Executable numpy model of the GPU algorithm (test infrastructure).
+
+Mirrors the index arithmetic of paper_2201_10473_b200/csrc kernels one to one
+so that the plan / layout logic can be checked on a CPU box against the
+oracle.  It is NOT an oracle (it is checked against one) and never runs on the
+product path.
+
+Stages:
+  k1  packed uint64[batch][t] -> bitsliced, chunked uint32[G][Ns]
+  k2  per (group, path): XOR-load of the path's operand segments, in-CTA
+      breadth-first Karatsuba (appended-mid layout), leaf schoolbook, in-place
+      interpolation -> node product
+  k3  global interpolation passes (elementwise over the quarter index)
+  k4  fold mod X^n-1 (cyclic) + transpose back to packed uint64
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def pow3(k: int) -> int:
+    return 3 ** k
+
+
+def transpose32(x: np.ndarray) -> np.ndarray:
+    """x: uint32[32, ...] -> y with bit p of y[i] = bit i of x[p]."""
+    x = x.astype(np.uint32).copy()
+    j, m = 16, np.uint32(0x0000FFFF)
+    while j:
+        for k in range(32):
+            if k & j == 0:
+                t = ((x[k] >> np.uint32(j)) ^ x[k + j]) & m
+                x[k + j] ^= t
+                x[k] ^= (t << np.uint32(j)).astype(np.uint32)
+        j //= 2
+        if j:
+            m = m ^ np.uint32((int(m) << j) & 0xFFFFFFFF)
+    return x
+
+
+class Plan:
+    def __init__(self, LF: int, K: int, KC: int, *, kind: str, t: int, n: int, batch: int):
+        self.LF, self.K, self.KC = LF, K, KC
+        self.GL = K - KC
+        self.LFS = (LF + 3) & ~3
+        self.N = LF << K            # logical coefficients per operand
+        self.Ns = self.LFS << K     # storage words per operand per group
+        self.S = LF << KC
+        self.Ss = self.LFS << KC
+        self.kind, self.t, self.n, self.batch = kind, t, n, batch
+        self.G = (batch + 31) // 32
+        assert self.N >= 64 * t
+
+    def idx(self, k):
+        return (k // self.LF) * self.LFS + k % self.LF
+
+
+def k1(plan: Plan, X: np.ndarray) -> np.ndarray:
+    G, t = plan.G, plan.t
+    out = np.zeros((G, plan.Ns), dtype=np.uint32)
+    Xp = np.zeros((G * 32, t), dtype=np.uint64)
+    Xp[: X.shape[0]] = X
+    lo = (Xp & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    hi = (Xp >> np.uint64(32)).astype(np.uint32)
+    for g in range(G):
+        for u in range((plan.N + 63) // 64):
+            if u < t:
+                ylo = transpose32(lo[32 * g: 32 * g + 32, u])
+                yhi = transpose32(hi[32 * g: 32 * g + 32, u])
+                words = np.concatenate([ylo, yhi])
+            else:
+                words = np.zeros(64, dtype=np.uint32)
+            for i in range(64):
+                k = 64 * u + i
+                if k < plan.N:
+                    out[g, plan.idx(k)] = words[i]
+    return out
+
+
+def leaf_positions(plan: Plan):
+    """P_j(nu) in words for j = 0..KC; R_j = LFS * 2^(KC-j) * 3^j."""
+    KC, LFS = plan.KC, plan.LFS
+    P = [[0]]
+    for j in range(1, KC + 1):
+        hq = LFS << (KC - j)          # half of a level-(j-1) node
+        R = LFS * (2 ** (KC - j + 1)) * pow3(j - 1)
+        cur = []
+        for nu in range(pow3(j)):
+            par, d = divmod(nu, 3)
+            p = P[j - 1][par]
+            cur.append(p if d == 0 else p + hq if d == 1 else R + par * hq)
+        P.append(cur)
+    return P
+
+
+def path_segments(plan: Plan, path: int):
+    """Chunk offsets of the segments XORed into the path's operand."""
+    GL, K = plan.GL, plan.K
+    digits = []
+    for _ in range(GL):
+        path, d = divmod(path, 3)
+        digits.append(d)
+    digits = digits[::-1]  # most significant = top level
+    base, mids = 0, []
+    for j, d in enumerate(digits, start=1):
+        hc = 1 << (K - j)
+        if d == 1:
+            base += hc
+        elif d == 2:
+            mids.append(hc)
+    offs = []
+    for mask in range(1 << len(mids)):
+        o = base + sum(m for b, m in enumerate(mids) if mask >> b & 1)
+        offs.append(o)
+    return offs
+
+
+def k2(plan: Plan, Abs: np.ndarray, Bbs: np.ndarray) -> np.ndarray:
+    LF, LFS, KC, GL, Ss = plan.LF, plan.LFS, plan.KC, plan.GL, plan.Ss
+    R = LFS * pow3(KC)  # region words
+    P = leaf_positions(plan)
+    out = np.zeros((plan.G, pow3(GL), 2 * Ss), dtype=np.uint32)
+    for g in range(plan.G):
+        for path in range(pow3(GL)):
+            As = np.zeros(R, dtype=np.uint32)
+            Bs = np.zeros(R, dtype=np.uint32)
+            for o in path_segments(plan, path):
+                As[:Ss] ^= Abs[g, o * LFS: o * LFS + Ss]
+                Bs[:Ss] ^= Bbs[g, o * LFS: o * LFS + Ss]
+            # eval
+            for j in range(KC):
+                h = LFS << (KC - j - 1)
+                Rj = LFS * (2 ** (KC - j)) * pow3(j)
+                for it in range(pow3(j) * h):
+                    nu, u = divmod(it, h)
+                    s = P[j][nu]
+                    As[Rj + it] = As[s + u] ^ As[s + h + u]
+                    Bs[Rj + it] = Bs[s + u] ^ Bs[s + h + u]
+            # leaves
+            for leaf in range(pow3(KC)):
+                p = P[KC][leaf]
+                a = As[p: p + LF].astype(np.uint32)
+                b = Bs[p: p + LF].astype(np.uint32)
+                c = np.zeros(2 * LF, dtype=np.uint32)
+                for i in range(LF):
+                    c[i: i + LF] ^= a[i] & b
+                As[p: p + LFS] = 0
+                Bs[p: p + LFS] = 0
+                As[p: p + LF] = c[:LF]
+                Bs[p: p + LF] = c[LF:]
+            # interp
+            for j in range(KC - 1, -1, -1):
+                h = LFS << (KC - j - 1)
+                Rj = LFS * (2 ** (KC - j)) * pow3(j)
+                for it in range(pow3(j) * h):
+                    nu, u = divmod(it, h)
+                    s = P[j][nu]
+                    L0, H0 = As[s + u], Bs[s + u]
+                    L1, H1 = As[s + h + u], Bs[s + h + u]
+                    Ml, Mh = As[Rj + it], Bs[Rj + it]
+                    T = H0 ^ L1
+                    As[s + h + u] = T ^ L0 ^ Ml
+                    Bs[s + u] = T ^ H1 ^ Mh
+            out[g, path, :Ss] = As[:Ss]
+            out[g, path, Ss:] = Bs[:Ss]
+    return out
+
+
+def k3_pass(plan: Plan, Pin: np.ndarray, d_hi: int, glp: int) -> np.ndarray:
+    d_lo = d_hi - glp
+    S_hi = plan.Ns >> d_hi
+    qw = S_hi // 2
+    G = plan.G
+
+    def rec(D, desc, g, w):
+        if D == 0:
+            return [Pin[g, desc, q * qw + w] for q in range(4)]
+        out = rec(D - 1, desc * 3 + 0, g, w) + rec(D - 1, desc * 3 + 1, g, w)
+        m = rec(D - 1, desc * 3 + 2, g, w)
+        Lc = 2 << D
+        half = Lc // 2
+        for i in range(half):
+            T = out[half + i] ^ out[Lc + i]
+            out[half + i] = T ^ out[i] ^ m[i]
+            out[Lc + i] = T ^ out[Lc + half + i] ^ m[half + i]
+        return out
+
+    Pout = np.zeros((G, pow3(d_lo), 2 * (plan.Ns >> d_lo)), dtype=np.uint32)
+    for g in range(G):
+        for nu in range(pow3(d_lo)):
+            for w in range(qw):
+                v = rec(glp, nu, g, w)
+                for m_, val in enumerate(v):
+                    Pout[g, nu, m_ * qw + w] = val
+    return Pout
+
+
+def k4(plan: Plan, C: np.ndarray) -> np.ndarray:
+    """C: uint32[G][2Ns] root product (chunked)."""
+    t, n, batch = plan.t, plan.n, plan.batch
+    tout = 2 * t if plan.kind == "full" else t
+    out = np.zeros((batch, tout), dtype=np.uint64)
+    for g in range(plan.G):
+        for u in range(tout):
+            words = np.zeros(64, dtype=np.uint32)
+            for i in range(64):
+                k = 64 * u + i
+                if plan.kind == "full":
+                    words[i] = C[g, plan.idx(k)]
+                elif k < n:
+                    words[i] = C[g, plan.idx(k)] ^ C[g, plan.idx(k + n)]
+            lo = transpose32(words[:32])
+            hi = transpose32(words[32:])
+            for p in range(32):
+                if 32 * g + p < batch:
+                    out[32 * g + p, u] = np.uint64(lo[p]) | (np.uint64(hi[p]) << np.uint64(32))
+    return out
+
+
+def split_passes(GL: int, maxp: int = 3):
+    passes = []
+    rem = GL
+    while rem > 0:
+        p = min(maxp, rem)
+        passes.append(p)
+        rem -= p
+    return passes  # bottom first
+
+
+def run(plan: Plan, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    Abs = k1(plan, A)
+    Bbs = k1(plan, B)
+    P = k2(plan, Abs, Bbs)
+    d = plan.GL
+    for glp in split_passes(plan.GL):
+        P = k3_pass(plan, P, d, glp)
+        d -= glp
+    return k4(plan, P[:, 0, :])

@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle and the golden
+vectors produced by the real reference.  Bit-exact on every word."""
+
+import numpy as np
+import pytest
+
+from conftest import int_clmul
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(x, cuda):
+    """Device copy as int64 words (same bits; torch's uint64 kernels are thin)."""
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64).view(np.int64)).to(cuda)
+
+
+def _np(x):
+    return x.cpu().numpy().view(np.uint64)
+
+
+# ---------------------------------------------------------------- golden pins
+
+def test_golden_full(golden, cuda):
+    from paper_2201_10473_b200 import mul_full
+
+    for t in golden["full_ts"]:
+        A, B, C = golden[f"full_t{t}_A"], golden[f"full_t{t}_B"], golden[f"full_t{t}_C"]
+        out = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+        assert np.array_equal(out, C), f"t={t}"
+
+
+def test_golden_cyclic(golden, cuda):
+    from paper_2201_10473_b200 import mul_cyclic
+
+    for n in golden["cyc_ns"]:
+        A, B, C = golden[f"cyc_n{n}_A"], golden[f"cyc_n{n}_B"], golden[f"cyc_n{n}_C"]
+        out = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), int(n)))
+        assert np.array_equal(out, C), f"n={n}"
+
+
+def test_golden_clmul_lanes(golden, cuda):
+    from paper_2201_10473_b200 import clmul64_batch
+
+    lo, hi = clmul64_batch(golden["clmul_a"], golden["clmul_b"])
+    assert np.array_equal(lo, golden["clmul_lo"])
+    assert np.array_equal(hi, golden["clmul_hi"])
+
+
+# ------------------------------------------------- oracle at config sizes
+
+@pytest.mark.parametrize("n,batch", [(12323, 256), (17669, 96), (35851, 64), (57637, 40)])
+def test_cyclic_configs_vs_oracle(n, batch, cuda):
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    A, B = make_cyclic_inputs(n, batch)
+    out = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), n))
+    assert np.array_equal(out, c_mul_cyclic(A, B, n))
+
+
+@pytest.mark.parametrize("t", [1, 2, 3, 16, 17, 33, 64, 100, 128, 256, 512, 1024])
+def test_full_sizes_vs_oracle(t, cuda):
+    from oracle import c_mul_full
+    from oracle.f2x_oracle import make_full_inputs
+    from paper_2201_10473_b200 import mul_full
+
+    batch = 70 if t <= 256 else 33
+    A, B = make_full_inputs(t, batch, words=True)
+    out = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+    assert np.array_equal(out, c_mul_full(A, B))
+
+
+@pytest.mark.parametrize("leaf", [16, 18, 23, 25, 29, 32, 35, 36, 40])
+def test_forced_leaf_sizes(leaf, cuda):
+    """Every leaf instantiation the planner can pick, on one ring size."""
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    n = 17669
+    A, B = make_cyclic_inputs(n, 33)
+    out = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), n, leaf=leaf))
+    assert np.array_equal(out, c_mul_cyclic(A, B, n))
+
+
+# ------------------------------------------------------------- edge cases
+
+def test_ragged_batches(cuda):
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    for batch in (1, 31, 32, 33, 65):
+        A, B = make_cyclic_inputs(1000, batch)
+        out = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), 1000))
+        assert np.array_equal(out, c_mul_cyclic(A, B, 1000)), batch
+
+
+def test_empty_batch(cuda):
+    import torch
+
+    from paper_2201_10473_b200 import mul_cyclic, mul_full
+
+    z = torch.zeros((0, 5), dtype=torch.int64, device=cuda)
+    assert mul_full(z, z).shape == (0, 10)
+    assert mul_cyclic(z, z, 300).shape == (0, 5)
+
+
+def test_top_bits_rejected(cuda):
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    n = 17669
+    A, B = make_cyclic_inputs(n, 40)
+    B[37, -1] |= np.uint64(1 << (n % 64))  # bit n set
+    with pytest.raises(ValueError):
+        mul_cyclic(_dev(A, cuda), _dev(B, cuda), n)
+    A2, _ = make_cyclic_inputs(n, 40)
+    A2[0, -1] |= np.uint64(1 << 63)
+    with pytest.raises(ValueError):
+        mul_cyclic(_dev(A2, cuda), _dev(A2, cuda), n)
+
+
+def test_shape_errors(cuda):
+    import torch
+
+    from paper_2201_10473_b200 import mul_cyclic, mul_full
+
+    a = torch.zeros((4, 3), dtype=torch.int64, device=cuda)
+    b = torch.zeros((4, 2), dtype=torch.int64, device=cuda)
+    with pytest.raises(ValueError):
+        mul_full(a, b)
+    with pytest.raises(ValueError):
+        mul_cyclic(a, a, 1000)  # needs 16 words
+    with pytest.raises(ValueError):
+        mul_full(a.cpu(), a.cpu())
+
+
+def test_ring_identities_all_presets(cuda):
+    """A*1 = A and X^(N-1)*X = 1, at the HQC sizes."""
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    for n in (17669, 35851, 57637):
+        t = (n + 63) // 64
+        A, _ = make_cyclic_inputs(n, 32)
+        one = np.zeros_like(A)
+        one[:, 0] = 1
+        assert np.array_equal(_np(mul_cyclic(_dev(A, cuda), _dev(one, cuda), n)), A)
+        xn1 = np.zeros((1, t), dtype=np.uint64)
+        xn1[0, (n - 1) // 64] = np.uint64(1 << ((n - 1) % 64))
+        x = np.zeros((1, t), dtype=np.uint64)
+        x[0, 0] = 2
+        r = _np(mul_cyclic(_dev(xn1, cuda), _dev(x, cuda), n))
+        expect = np.zeros((1, t), dtype=np.uint64)
+        expect[0, 0] = 1
+        assert np.array_equal(r, expect)
+
+
+# ------------------------------------- full-size properties (no oracle)
+
+@pytest.mark.parametrize("n,batch", [(17669, 4096), (35851, 4096), (57637, 2048)])
+def test_full_size_properties(n, batch, cuda):
+    """At BASELINE sizes: commutativity, bilinearity and cyclic == fold(full),
+    plus a 1-row-in-64 oracle subsample."""
+    import torch
+
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic, mul_full
+
+    A, B = make_cyclic_inputs(n, batch)
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    C = mul_cyclic(dA, dB, n)
+    assert torch.equal(C, mul_cyclic(dB, dA, n))
+    D = _dev(np.roll(B, 1, axis=0), cuda)
+    lhs = mul_cyclic(dA, dB ^ D, n)
+    rhs = mul_cyclic(dA, dB, n) ^ mul_cyclic(dA, D, n)
+    assert torch.equal(lhs, rhs)
+    # cyclic product equals the fold of the full product
+    sub = slice(0, batch, 64)
+    full = _np(mul_full(dA[sub].contiguous(), dB[sub].contiguous()))
+    from oracle.f2x_oracle import fold_cyclic
+
+    folded = np.stack([fold_cyclic(full[i], n) for i in range(full.shape[0])])
+    Cn = _np(C)
+    assert np.array_equal(Cn[sub], folded)
+    assert np.array_equal(Cn[sub], c_mul_cyclic(A[sub], B[sub], n))
+
+
+# ------------------------------------------------ reference-mirroring API
+
+def test_scalar_api_known_answers(cuda):
+    """The reference's own known answers (test_poly.py:134-143, 219-225)."""
+    from paper_2201_10473_b200 import PolyWords, WideProduct, clmul64, schoolbook_mul
+
+    assert clmul64(0x0, 0xDEADBEEF) == (0, 0)
+    assert clmul64(0x1, 0xFEDCBA9876543210) == (0xFEDCBA9876543210, 0)
+    assert clmul64(0x5, 0x3) == (0xF, 0)
+    r = schoolbook_mul(PolyWords([1]), PolyWords([1 << 63]))
+    assert isinstance(r, WideProduct) and r.word_len == 2 and r.to_int() == 1 << 63
+    with pytest.raises(ValueError):
+        schoolbook_mul(PolyWords([1]), PolyWords([1, 2]))
+    with pytest.raises(ValueError):
+        clmul64(1 << 64, 1)
+
+
+def test_scalar_api_vs_bitwise(rng, cuda):
+    from paper_2201_10473_b200 import PolyWords, clmul64, ring_mul, schoolbook_mul
+
+    for _ in range(20):
+        a, b = (int(x) for x in rng.integers(0, 1 << 64, 2, dtype=np.uint64))
+        lo, hi = clmul64(a, b)
+        assert lo | (hi << 64) == int_clmul(a, b)
+    a = PolyWords(rng.integers(0, 1 << 64, 4, dtype=np.uint64))
+    b = PolyWords(rng.integers(0, 1 << 64, 4, dtype=np.uint64))
+    assert schoolbook_mul(a, b).to_int() == int_clmul(a.to_int(), b.to_int())
+    n = 200
+    ai = int(rng.integers(0, 1 << 63)) << 100 | 12345
+    ai &= (1 << n) - 1
+    bi = (1 << 199) | 77
+    p = int_clmul(ai, bi)
+    want = (p & ((1 << n) - 1)) ^ (p >> n)
+    got = ring_mul(PolyWords.from_int(ai, 4), PolyWords.from_int(bi, 4), n)
+    assert got.to_int() == want
+
+
+def test_ring_weight75_dense_path(cuda):
+    """A weight-75 sparse first operand goes through the same
+    dense path and matches the oracle."""
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import sparse_to_dense
+
+    import torch
+
+    from paper_2201_10473_b200 import mul_cyclic
+
+    n = 17669
+    rng = np.random.default_rng(75)
+    rows = [sparse_to_dense(rng.choice(n, 75, replace=False), n).words for _ in range(32)]
+    A = np.stack(rows)
+    _, B = make_cyclic_inputs(n, 32)
+    out = mul_cyclic(_dev(A, cuda), _dev(B, cuda), n)
+    assert np.array_equal(_np(out), c_mul_cyclic(A, B, n))
