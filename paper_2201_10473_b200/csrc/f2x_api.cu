@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/f2x.h"
@@ -296,6 +297,24 @@ static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw,
     return 0;
 }
 
+// F2X_DEBUG_SYNC=1: synchronise after every launch and report the failing
+// stage (development aid; never set in benchmarks).
+static int debug_sync(cudaStream_t s, int stage) {
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char *v = getenv("F2X_DEBUG_SYNC");
+        enabled = v && v[0] == '1';
+    }
+    if (!enabled) return 0;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "f2x: stage %d failed: %s\n", stage, cudaGetErrorString(e));
+        return F2X_ECUDA - int(e);
+    }
+    return 0;
+}
+
 static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int64_t batch,
                int t_or_n, void *ws, size_t ws_bytes, int leaf_hint, uint32_t *d_err,
                cudaStream_t stream) {
@@ -324,6 +343,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         k1_slice<<<grid, kThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N, pl.leaf_words,
                                                 pl.leaf_stride, L.Ns, ncyc, d_err, UB, items);
     }
+    if ((rc = debug_sync(stream, 1))) return rc;
     // K2
     const K2Entry *e = find_k2(pl.leaf_words, pl.cta_levels);
     K2Params kp;
@@ -336,6 +356,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.paths = int(ipow3(pl.global_levels));
     rc = e->launch(kp, pl.node_ctas, stream);
     if (rc) return rc;
+    if ((rc = debug_sync(stream, 2))) return rc;
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
     int d = pl.global_levels;
@@ -351,6 +372,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             case 3: launch_k3<3>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             default: return F2X_ERANGE;
         }
+        if ((rc = debug_sync(stream, 3))) return rc;
         std::swap(cur, nxt);
         d = dlo;
     }
@@ -361,6 +383,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         k4_unslice<<<unsigned(ceil_div(items, kThreads)), kThreads, 0, stream>>>(
             cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, items);
     }
+    if ((rc = debug_sync(stream, 4))) return rc;
     const cudaError_t ce = cudaGetLastError();
     return ce == cudaSuccess ? F2X_OK : F2X_ECUDA - int(ce);
 }
