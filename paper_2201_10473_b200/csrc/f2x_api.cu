@@ -134,7 +134,7 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
     const int64_t node = item / qw;
     const int w = int(item - node * qw);
     uint32_t v[4 << D];
-    k3_rec<D>(v, Pin, inStride, node * pow3c(D), qw, w);
+    k3_rec<D>(v, Pin, inStride, node, qw, w);  // leaves: node*3^D + local
     uint32_t *dst = Pout + node * outStride + w;
 #pragma unroll
     for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qw] = v[m];
@@ -372,6 +372,13 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             case 3: launch_k3<3>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             default: return F2X_ERANGE;
         }
+        if (getenv("F2X_DEBUG_SYNC"))
+            fprintf(stderr, "f2x pass %d: D=%d d=%d dlo=%d qw=%d items=%lld inS=%lld outS=%lld "
+                    "cur=%s maxread=%lld maxwrite=%lld p0=%lld p1=%lld\n", i, D, d, dlo, qw,
+                    (long long)items, (long long)(2 * Shi), (long long)(2 * Slo),
+                    cur == P0 ? "P0" : "P1", (long long)(G * ipow3(d) * 2 * Shi),
+                    (long long)(G * ipow3(dlo) * 2 * Slo), (long long)((L.off_p1 - L.off_p0) / 4),
+                    (long long)((L.total - L.off_p1) / 4));
         if ((rc = debug_sync(stream, 3))) return rc;
         std::swap(cur, nxt);
         d = dlo;

@@ -12,6 +12,7 @@ if len(sys.argv) > 1:
     cfgs = [c for c in cfgs if str(c[1]) in sys.argv[1:]]
 leaf = int(os.environ.get("LEAF", "0"))
 for kind, size, batch in cfgs:
+    print("cfg", kind, size, batch, flush=True)
     if kind == "cyc":
         A, B = make_cyclic_inputs(size, min(batch, 4096))
     else:
