@@ -279,11 +279,20 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     const int64_t p0 = G * ipow3(GL) * 2 * L.Ss * 4;
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
-    if (np >= 2) {
+    if (np >= 1) {  // first pass output (the largest one written to P1)
         const int d1 = GL - pl->pass_levels[0];
         p1 = G * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
     L.total = align256(L.off_p1 + p1);
+    {  // every pass output must fit the ping-pong buffer it is written to
+        int d = GL;
+        for (int i = 0; i < np; ++i) {
+            const int dlo = d - pl->pass_levels[i];
+            const int64_t outb = G * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
+            if (outb > ((i & 1) ? p0 : p1)) return F2X_ERANGE;
+            d = dlo;
+        }
+    }
     pl->workspace_bytes = L.total;
     if (lay) *lay = L;
     return F2X_OK;
