@@ -101,6 +101,15 @@ F2X_API int f2x_mul_cyclic(const uint64_t *A, const uint64_t *B, uint64_t *C, in
 F2X_API int f2x_clmul64(const uint64_t *a, const uint64_t *b, uint64_t *lohi, int64_t lanes,
                 void *workspace, size_t workspace_bytes, void *stream);
 
+/* Measurement hooks (bench.py / profiling; not part of the reference API).
+ * f2x_set_node_events: cudaEvent_t pair recorded on the call's stream right
+ * before and after the node kernel of every later call from this thread
+ * (NULL, NULL disables).  f2x_bench_lop3: integer-ALU peak microbenchmark,
+ * blocks x 256 threads x iters x 128 LOP3 lane-ops; out needs
+ * blocks*256 uint32. */
+F2X_API int f2x_set_node_events(void *begin, void *end);
+F2X_API int f2x_bench_lop3(uint32_t *out, int32_t blocks, int32_t iters, void *stream);
+
 F2X_API const char *f2x_strerror(int code);
 F2X_API int f2x_version(void);
 

@@ -27,6 +27,8 @@ EXPORTS = (
     "f2x_mul_full",
     "f2x_mul_cyclic",
     "f2x_clmul64",
+    "f2x_set_node_events",
+    "f2x_bench_lop3",
     "f2x_strerror",
     "f2x_version",
 )
@@ -92,6 +94,10 @@ def load() -> ctypes.CDLL:
         lib.f2x_mul_cyclic.restype = ctypes.c_int
         lib.f2x_clmul64.argtypes = [vp, vp, vp, i64, vp, sz, vp]
         lib.f2x_clmul64.restype = ctypes.c_int
+        lib.f2x_set_node_events.argtypes = [vp, vp]
+        lib.f2x_set_node_events.restype = ctypes.c_int
+        lib.f2x_bench_lop3.argtypes = [vp, i32, i32, vp]
+        lib.f2x_bench_lop3.restype = ctypes.c_int
         lib.f2x_strerror.argtypes = [ctypes.c_int]
         lib.f2x_strerror.restype = ctypes.c_char_p
         lib.f2x_version.argtypes = []

@@ -306,6 +306,33 @@ static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw,
     return 0;
 }
 
+// Optional per-thread events recorded around the node kernel (bench.py uses
+// them to time the dominant kernel live on the launching stream).
+static thread_local cudaEvent_t g_node_ev[2] = {nullptr, nullptr};
+
+// Integer-ALU peak microbenchmark: 8 independent chains per thread of the
+// leaf's exact instruction, d = c ^ (a & b) (LOP3 LUT 0x6A), 16 distinct
+// operands so nothing folds.  lane-ops = blocks*threads*iters*128.
+__global__ void __launch_bounds__(256) lop3_peak(uint32_t *out, int iters, uint32_t seed) {
+    uint32_t acc[8], x[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = seed * (i + 1) + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = (seed + 0x9E3779B9u * k) ^ (blockIdx.x << 5);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile("lop3.b32 %0, %1, %2, %0, 0x6A;" : "+r"(acc[i]) : "r"(x[k]), "r"(x[(k + i + 1) & 15]));
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r ^= acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
 // F2X_DEBUG_SYNC=1: synchronise after every launch and report the failing
 // stage (development aid; never set in benchmarks).
 static int debug_sync(cudaStream_t s, int stage) {
@@ -363,8 +390,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.K = pl.levels;
     kp.GL = pl.global_levels;
     kp.paths = int(ipow3(pl.global_levels));
+    if (g_node_ev[0]) cudaEventRecord(g_node_ev[0], stream);
     rc = e->launch(kp, pl.node_ctas, stream);
     if (rc) return rc;
+    if (g_node_ev[1]) cudaEventRecord(g_node_ev[1], stream);
     if ((rc = debug_sync(stream, 2))) return rc;
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
@@ -437,6 +466,19 @@ int f2x_clmul64(const uint64_t *a, const uint64_t *b, uint64_t *lohi, int64_t la
                 void *workspace, size_t workspace_bytes, void *stream) {
     return f2x::run(F2X_KIND_FULL, a, b, lohi, lanes, 1, workspace, workspace_bytes, 0, nullptr,
                     static_cast<cudaStream_t>(stream));
+}
+
+int f2x_set_node_events(void *begin, void *end) {
+    f2x::g_node_ev[0] = static_cast<cudaEvent_t>(begin);
+    f2x::g_node_ev[1] = static_cast<cudaEvent_t>(end);
+    return F2X_OK;
+}
+
+int f2x_bench_lop3(uint32_t *out, int32_t blocks, int32_t iters, void *stream) {
+    if (!out || blocks < 1 || iters < 1) return F2X_EINVAL;
+    f2x::lop3_peak<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0x1234567u);
+    const cudaError_t ce = cudaGetLastError();
+    return ce == cudaSuccess ? F2X_OK : F2X_ECUDA - int(ce);
 }
 
 const char *f2x_strerror(int code) {
