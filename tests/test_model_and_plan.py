@@ -1,0 +1,152 @@
+"""CPU checks of the GPU algorithm's index math and of the host planner.
+
+``model_bitsliced`` executes the kernels' exact layout/index arithmetic in
+numpy; it is compared with the oracle here, so plan/layout bugs show up
+without a GPU.  The planner is exercised through the real C ABI (libf2x.so
+loads and plans without a device).
+"""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import model_bitsliced as mb
+from oracle import f2x_oracle as o
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("kind,t,n,LF,K,KC,batch", [
+    ("full", 1, 0, 16, 2, 2, 5),
+    ("full", 2, 0, 17, 3, 2, 33),
+    ("full", 4, 0, 19, 4, 2, 40),
+    ("full", 8, 0, 16, 5, 1, 2),       # GL=4: passes [3, 1]
+    ("cyc", 0, 100, 16, 3, 1, 3),
+    ("cyc", 0, 129, 13, 4, 2, 3),
+    ("cyc", 0, 300, 10, 5, 3, 7),
+    ("cyc", 0, 300, 10, 5, 0, 2),      # GL=5: passes [3, 2]
+    ("full", 4, 0, 2, 7, 0, 1),        # GL=7: passes [3, 3, 1]
+])
+def test_model_matches_oracle(kind, t, n, LF, K, KC, batch):
+    rng = np.random.default_rng(LF * 1000 + K)
+    if kind == "full":
+        A = rng.integers(0, 1 << 64, (batch, t), dtype=np.uint64)
+        B = rng.integers(0, 1 << 64, (batch, t), dtype=np.uint64)
+        p = mb.Plan(LF, K, KC, kind="full", t=t, n=0, batch=batch)
+        ref = o.mul_full(A, B)
+    else:
+        A, B = o.make_cyclic_inputs(n, batch)
+        t = A.shape[1]
+        p = mb.Plan(LF, K, KC, kind="cyc", t=t, n=n, batch=batch)
+        ref = o.mul_cyclic(A, B, n)
+    assert np.array_equal(mb.run(p, A, B), ref)
+
+
+def test_position_table_matches_generator():
+    """The kernels' precomputed table (gen_instances.py) equals the model's."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "gen", os.path.join(ROOT, "paper_2201_10473_b200", "csrc", "gen_instances.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    for KC in range(6):
+        plan = mb.Plan(1, KC, KC, kind="full", t=0, n=0, batch=1)
+        plan.LFS = 1  # positions in chunks
+        flat = [x for lvl in mb.leaf_positions(plan) for x in lvl]
+        assert gen.pos_table(KC) == flat
+
+
+def test_transpose_model():
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 1 << 32, 32, dtype=np.uint64).astype(np.uint32)
+    y = mb.transpose32(x)
+    for i in range(32):
+        for p in range(32):
+            assert (int(y[i]) >> p) & 1 == (int(x[p]) >> i) & 1
+
+
+# ----------------------------------------------------------- C ABI on CPU
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2201_10473_b200 import _lib
+
+    try:
+        return _lib.load()
+    except ImportError:
+        from paper_2201_10473_b200 import build
+
+        build.build()
+        return _lib.load()
+
+
+def test_abi_exports_every_declared_symbol(lib):
+    from paper_2201_10473_b200 import _lib
+
+    hdr = open(os.path.join(ROOT, "include", "f2x.h")).read()
+    import re
+
+    declared = set(re.findall(r"F2X_API\s+[\w\s\*]+?\b(f2x_\w+)\s*\(", hdr))
+    assert declared == set(_lib.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert declared <= exported, declared - exported
+    for name in declared:
+        assert hasattr(lib, name)
+
+
+def test_plan_struct_size_matches_header(lib):
+    """ctypes mirror of f2x_plan must have the C layout (field offsets)."""
+    from paper_2201_10473_b200 import _lib
+
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)
+    assert pl.t == 277 and pl.n == 17669 and pl.groups == 128
+    assert pl.N >= 64 * 277 and pl.N == pl.leaf_words << pl.levels
+    assert pl.levels == pl.cta_levels + pl.global_levels
+    assert sum(pl.pass_levels[: pl.num_passes]) == pl.global_levels
+    assert pl.launches == 3 + pl.num_passes
+    assert pl.workspace_bytes > 0
+
+
+@pytest.mark.parametrize("t", list(range(1, 70)) + [100, 128, 193, 256, 277, 512, 561, 901, 1024, 2048])
+def test_plan_covers_every_size(lib, t):
+    from paper_2201_10473_b200 import _lib
+
+    pl = _lib.make_plan(_lib.KIND_FULL, 33, t)
+    assert pl.N >= 64 * t
+    assert pl.N <= 64 * t * 1.25 + 64 * 16  # no pathological padding
+    assert 16 <= pl.leaf_words <= 40
+    assert pl.leaf_stride % 4 == 0 and pl.leaf_stride - pl.leaf_words < 4
+
+
+def test_plan_errors(lib):
+    from paper_2201_10473_b200 import _lib
+
+    with pytest.raises(ValueError):
+        _lib.make_plan(_lib.KIND_FULL, 0, 5)
+    with pytest.raises(ValueError):
+        _lib.make_plan(_lib.KIND_FULL, 1, 0)
+    with pytest.raises(ValueError):
+        _lib.make_plan(7, 1, 5)
+    with pytest.raises(ValueError):
+        _lib.make_plan(_lib.KIND_FULL, 1, 1 << 22)  # outside the envelope
+    assert "workspace" in _lib.strerror(_lib.F2X_ENOSPC)
+
+
+def test_null_pointer_rejected_without_gpu(lib):
+    rc = lib.f2x_mul_full(None, None, None, 1, 1, None, 0, 0, None)
+    assert rc == -22
+    rc = lib.f2x_mul_cyclic(None, None, None, 1, 100, None, 0, 0, None, None)
+    assert rc == -22
+
+
+def test_workspace_query(lib):
+    a = lib.f2x_workspace_bytes(1, 4096, 17669, 0)
+    b = lib.f2x_workspace_bytes(1, 8192, 17669, 0)
+    assert 0 < a < b
+    assert lib.f2x_workspace_bytes(1, 4096, 17669, 18) > 0
