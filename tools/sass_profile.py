@@ -32,3 +32,14 @@ reg.sort(key=lambda r: -(r[2] * r[4]))
 for a, b, ex, st, cnt in reg[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
     ops = collections.Counter(data[j][1].split(".")[0] for j in range(a, b + 1))
     print(f"[{a:5d}-{b:5d}] n={cnt:5d} exec/instr={ex:>10,} total={ex*cnt:>13,} stall={100*st/max(tot_st,1):5.1f}% ops={dict(ops.most_common(5))}")
+
+# stall reasons per address range: python sass_profile.py dump.csv N lo-hi ...
+reasons = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
+for rng_ in sys.argv[3:]:
+    lo, hi = map(int, rng_.split("-"))
+    tot = collections.Counter()
+    for r in rows[2 + lo: 2 + hi + 1]:
+        for c in reasons:
+            tot[c] += int(r[ix[c]] or 0)
+    s = sum(tot.values()) or 1
+    print(f"[{lo}-{hi}] samples {s}: " + ", ".join(f"{k[6:]} {100*v/s:.0f}%" for k, v in tot.most_common(6)))
