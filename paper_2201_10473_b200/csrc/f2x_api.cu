@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/f2x.h"
 #include "f2x_kernels.cuh"
@@ -390,10 +391,31 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.K = pl.levels;
     kp.GL = pl.global_levels;
     kp.paths = int(ipow3(pl.global_levels));
+    kp.prof = nullptr;
+    const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
+    if (prof_path) cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
     if (g_node_ev[0]) cudaEventRecord(g_node_ev[0], stream);
     rc = e->launch(kp, pl.node_ctas, stream);
     if (rc) return rc;
     if (g_node_ev[1]) cudaEventRecord(g_node_ev[1], stream);
+    if (kp.prof) {
+        std::vector<long long> h(size_t(pl.node_ctas) * 8);
+        cudaStreamSynchronize(stream);
+        cudaMemcpy(h.data(), kp.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        cudaFree(kp.prof);
+        double acc[7] = {0};
+        long long t0 = h[0], t1 = h[6];
+        for (int64_t b = 0; b < pl.node_ctas; ++b)
+            for (int i = 0; i < 6; ++i) acc[i] += double(h[b * 8 + i + 1] - h[b * 8 + i]);
+        FILE *f = fopen(prof_path, "a");
+        if (f) {
+            fprintf(f, "LF=%d KC=%d GL=%d ctas=%lld avg cycles: setup %.0f load %.0f eval %.0f leaf %.0f interp %.0f store %.0f (first cta total %lld)\n",
+                    pl.leaf_words, pl.cta_levels, pl.global_levels, (long long)pl.node_ctas,
+                    acc[0] / pl.node_ctas, acc[1] / pl.node_ctas, acc[2] / pl.node_ctas,
+                    acc[3] / pl.node_ctas, acc[4] / pl.node_ctas, acc[5] / pl.node_ctas, t1 - t0);
+            fclose(f);
+        }
+    }
     if ((rc = debug_sync(stream, 2))) return rc;
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
