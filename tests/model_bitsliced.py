@@ -237,3 +237,135 @@ def run(plan: Plan, A: np.ndarray, B: np.ndarray) -> np.ndarray:
         P = k3_pass(plan, P, d, glp)
         d -= glp
     return k4(plan, P[:, 0, :])
+
+
+# ---------------------------------------------------------------------------
+# v2 node schedule (mirrors the current kernel): eval levels 0..KC-2 in merged
+# pairs (4 loads -> 5 stores per quarter index), the bottom eval level fused
+# into the leaves (a mid leaf XORs its parent's two chunks while loading),
+# interpolation in merged pairs from the bottom, in place.
+
+def eval_pair(As, Bs, P, LFS, KC, j):
+    """Levels j and j+1 at once for every level-j node (needs j+1 <= KC-1)."""
+    q = LFS << (KC - j - 2)                     # quarter of a level-j node
+    Rj = LFS * (2 ** (KC - j)) * pow3(j)
+    Rj1 = LFS * (2 ** (KC - j - 1)) * pow3(j + 1)
+    for nu in range(pow3(j)):
+        p = P[j][nu]
+        for X in (As, Bs):
+            x0 = X[p: p + q].copy(); x1 = X[p + q: p + 2 * q].copy()
+            x2 = X[p + 2 * q: p + 3 * q].copy(); x3 = X[p + 3 * q: p + 4 * q].copy()
+            m0, m1 = x0 ^ x2, x1 ^ x3
+            X[Rj + nu * 2 * q: Rj + nu * 2 * q + q] = m0
+            X[Rj + nu * 2 * q + q: Rj + nu * 2 * q + 2 * q] = m1
+            X[Rj1 + (3 * nu) * q: Rj1 + (3 * nu + 1) * q] = x0 ^ x1
+            X[Rj1 + (3 * nu + 1) * q: Rj1 + (3 * nu + 2) * q] = x2 ^ x3
+            X[Rj1 + (3 * nu + 2) * q: Rj1 + (3 * nu + 3) * q] = m0 ^ m1
+
+
+def eval_single(As, Bs, P, LFS, KC, j):
+    h = LFS << (KC - j - 1)
+    Rj = LFS * (2 ** (KC - j)) * pow3(j)
+    for nu in range(pow3(j)):
+        s = P[j][nu]
+        for X in (As, Bs):
+            X[Rj + nu * h: Rj + (nu + 1) * h] = X[s: s + h] ^ X[s + h: s + 2 * h]
+
+
+def interp_single(As, Bs, P, LFS, KC, j):
+    h = LFS << (KC - j - 1)
+    Rj = LFS * (2 ** (KC - j)) * pow3(j)
+    for nu in range(pow3(j)):
+        s = P[j][nu]
+        L0, H0 = As[s: s + h].copy(), Bs[s: s + h].copy()
+        L1, H1 = As[s + h: s + 2 * h].copy(), Bs[s + h: s + 2 * h].copy()
+        Ml, Mh = As[Rj + nu * h: Rj + (nu + 1) * h].copy(), Bs[Rj + nu * h: Rj + (nu + 1) * h].copy()
+        T = H0 ^ L1
+        As[s + h: s + 2 * h] = T ^ L0 ^ Ml
+        Bs[s: s + h] = T ^ H1 ^ Mh
+
+
+def interp_pair(As, Bs, P, LFS, KC, j):
+    """Levels j+1 and j at once for every level-j node (j+1 <= KC-1), per
+    quarter index w: 18 reads (grandchildren halves), 6 writes, in place."""
+    q = LFS << (KC - j - 2)
+    for nu in range(pow3(j)):
+        kids = [3 * nu, 3 * nu + 1, 3 * nu + 2]
+        Qs = []
+        for kappa in kids:
+            pk = P[j + 1][kappa]
+            g0, g1, g2 = P[j + 2][3 * kappa], P[j + 2][3 * kappa + 1], P[j + 2][3 * kappa + 2]
+            L0, H0 = As[g0: g0 + q].copy(), Bs[g0: g0 + q].copy()
+            L1, H1 = As[g1: g1 + q].copy(), Bs[g1: g1 + q].copy()
+            Ml, Mh = As[g2: g2 + q].copy(), Bs[g2: g2 + q].copy()
+            T = H0 ^ L1
+            Qs.append((L0, T ^ L0 ^ Ml, T ^ H1 ^ Mh, H1, pk))
+        (c0q0, c0q1, c0q2, c0q3, p0), (c1q0, c1q1, c1q2, c1q3, p1), (c2q0, c2q1, c2q2, c2q3, _) = Qs
+        T0 = c0q2 ^ c1q0
+        T1 = c0q3 ^ c1q1
+        As[p0 + q: p0 + 2 * q] = c0q1
+        As[p1: p1 + q] = T0 ^ c0q0 ^ c2q0
+        As[p1 + q: p1 + 2 * q] = T1 ^ c0q1 ^ c2q1
+        Bs[p0: p0 + q] = T0 ^ c1q2 ^ c2q2
+        Bs[p0 + q: p0 + 2 * q] = T1 ^ c1q3 ^ c2q3
+        Bs[p1: p1 + q] = c1q2
+
+
+def k2_v2(plan: Plan, Abs: np.ndarray, Bbs: np.ndarray) -> np.ndarray:
+    LF, LFS, KC, GL, Ss = plan.LF, plan.LFS, plan.KC, plan.GL, plan.Ss
+    R = LFS * pow3(KC)
+    P = leaf_positions(plan)
+    out = np.zeros((plan.G, pow3(GL), 2 * Ss), dtype=np.uint32)
+    for g in range(plan.G):
+        for path in range(pow3(GL)):
+            As = np.zeros(R, dtype=np.uint32)
+            Bs = np.zeros(R, dtype=np.uint32)
+            for o in path_segments(plan, path):
+                As[:Ss] ^= Abs[g, o * LFS: o * LFS + Ss]
+                Bs[:Ss] ^= Bbs[g, o * LFS: o * LFS + Ss]
+            n_ev = KC - 1                       # levels evaluated in smem
+            j = 0
+            while j + 1 < n_ev:
+                eval_pair(As, Bs, P, LFS, KC, j)
+                j += 2
+            if j < n_ev:
+                eval_single(As, Bs, P, LFS, KC, j)
+            # leaves, one per chunk; a mid leaf (chunk >= R_{KC-1}) XORs its
+            # parent's two chunks (bottom eval level fused)
+            Rm = (R // LFS) - pow3(KC - 1) if KC >= 1 else R // LFS
+            prods = {}
+            for ch in range(R // LFS):
+                if KC >= 1 and ch >= Rm:
+                    pp = P[KC - 1][ch - Rm]
+                    a = As[pp: pp + LF] ^ As[pp + LFS: pp + LFS + LF]
+                    b = Bs[pp: pp + LF] ^ Bs[pp + LFS: pp + LFS + LF]
+                else:
+                    a = As[ch * LFS: ch * LFS + LF].copy()
+                    b = Bs[ch * LFS: ch * LFS + LF].copy()
+                c = np.zeros(2 * LF, dtype=np.uint32)
+                for i in range(LF):
+                    c[i: i + LF] ^= a[i] & b
+                prods[ch] = c
+            for ch, c in prods.items():   # written after all reads (barrier)
+                As[ch * LFS: (ch + 1) * LFS] = 0
+                Bs[ch * LFS: (ch + 1) * LFS] = 0
+                As[ch * LFS: ch * LFS + LF] = c[:LF]
+                Bs[ch * LFS: ch * LFS + LF] = c[LF:]
+            j = KC - 2
+            while j >= 0:
+                interp_pair(As, Bs, P, LFS, KC, j)
+                j -= 2
+            if j == -1:
+                interp_single(As, Bs, P, LFS, KC, 0)
+            out[g, path, :Ss] = As[:Ss]
+            out[g, path, Ss:] = Bs[:Ss]
+    return out
+
+
+def run_v2(plan: Plan, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    P = k2_v2(plan, k1(plan, A), k1(plan, B))
+    d = plan.GL
+    for glp in split_passes(plan.GL):
+        P = k3_pass(plan, P, d, glp)
+        d -= glp
+    return k4(plan, P[:, 0, :])
