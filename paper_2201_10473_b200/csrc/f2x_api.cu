@@ -393,7 +393,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.paths = int(ipow3(pl.global_levels));
     kp.prof = nullptr;
     const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
-    if (prof_path) cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
+    if (prof_path) {
+        cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
+        cudaMemset(kp.prof, 0, size_t(pl.node_ctas) * 8 * sizeof(long long));
+    }
     if (g_node_ev[0]) cudaEventRecord(g_node_ev[0], stream);
     rc = e->launch(kp, pl.node_ctas, stream);
     if (rc) return rc;
@@ -408,6 +411,19 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         for (int64_t b = 0; b < pl.node_ctas; ++b)
             for (int i = 0; i < 6; ++i) acc[i] += double(h[b * 8 + i + 1] - h[b * 8 + i]);
         FILE *f = fopen(prof_path, "a");
+        if (f && h[7] < 0) {  // warp-specialised kernel: per-CTA accumulated cycles
+            double a[5] = {0};
+            long long nodes = 0;
+            int rows = 0;
+            for (int64_t b = 0; b < pl.node_ctas && h[b * 8 + 7] < 0; ++b, ++rows) {
+                for (int i = 0; i < 5; ++i) a[i] += double(h[b * 8 + i]);
+                nodes += -h[b * 8 + 7];
+            }
+            fprintf(f, "WS LF=%d ctas=%d nodes=%lld per node: tree load+eval %.0f, tree wait %.0f, tree interp+store %.0f | leaf wait %.0f, leaves %.0f\n",
+                    pl.leaf_words, rows, nodes, a[0] / nodes, a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes);
+            fclose(f);
+            f = nullptr;
+        }
         if (f) {
             fprintf(f, "LF=%d KC=%d GL=%d ctas=%lld avg cycles: setup %.0f load %.0f eval %.0f leaf %.0f interp %.0f store %.0f (first cta total %lld)\n",
                     pl.leaf_words, pl.cta_levels, pl.global_levels, (long long)pl.node_ctas,
