@@ -60,7 +60,7 @@ typedef struct f2x_plan {
     int64_t batch;
     int64_t groups;          /* ceil(batch / 32)                              */
     int32_t leaf_words;      /* LF                                            */
-    int32_t leaf_stride;     /* LF rounded up to 4 (storage chunk)            */
+    int32_t leaf_stride;     /* chunk stride: 4 x odd #quads >= LF words     */
     int32_t levels;          /* K = global_levels + cta_levels                */
     int32_t cta_levels;      /* KC                                            */
     int32_t global_levels;   /* GL                                            */

@@ -233,7 +233,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     if (!bestLF) return F2X_ERANGE;
     const int LF = bestLF, K = bestK, KC = std::min(K, kMaxKC), GL = K - KC;
     const K2Entry *e = find_k2(LF, KC);
-    const int LFS = (LF + 3) & ~3;
+    const int LFS = leaf_stride_words(LF);
 
     pl->kind = kind;
     pl->t = t;

@@ -43,7 +43,8 @@ class Plan:
     def __init__(self, LF: int, K: int, KC: int, *, kind: str, t: int, n: int, batch: int):
         self.LF, self.K, self.KC = LF, K, KC
         self.GL = K - KC
-        self.LFS = (LF + 3) & ~3
+        q = (LF + 3) // 4
+        self.LFS = 4 * (q if q % 2 else q + 1)  # odd number of quads per chunk
         self.N = LF << K            # logical coefficients per operand
         self.Ns = self.LFS << K     # storage words per operand per group
         self.S = LF << KC

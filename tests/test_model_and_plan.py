@@ -29,6 +29,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     ("cyc", 0, 300, 10, 5, 3, 7),
     ("cyc", 0, 300, 10, 5, 0, 2),      # GL=5: passes [3, 2]
     ("full", 4, 0, 2, 7, 0, 1),        # GL=7: passes [3, 3, 1]
+    ("full", 4, 0, 9, 5, 5, 2),        # KC=5: eval pairs (0,1),(2,3); interp pairs 3,1 + level 0
+    ("full", 4, 0, 9, 5, 4, 2),        # KC=4: eval pair + single; interp pairs 2,0
+    ("full", 8, 0, 17, 5, 4, 1),
 ])
 def test_model_matches_oracle(kind, t, n, LF, K, KC, batch):
     rng = np.random.default_rng(LF * 1000 + K)
@@ -43,6 +46,7 @@ def test_model_matches_oracle(kind, t, n, LF, K, KC, batch):
         p = mb.Plan(LF, K, KC, kind="cyc", t=t, n=n, batch=batch)
         ref = o.mul_cyclic(A, B, n)
     assert np.array_equal(mb.run(p, A, B), ref)
+    assert np.array_equal(mb.run_v2(p, A, B), ref)  # the kernels' current schedule
 
 
 def test_position_table_matches_generator():
@@ -121,7 +125,8 @@ def test_plan_covers_every_size(lib, t):
     assert pl.N >= 64 * t
     assert pl.N <= 64 * t * 1.25 + 64 * 16  # no pathological padding
     assert 16 <= pl.leaf_words <= 40
-    assert pl.leaf_stride % 4 == 0 and pl.leaf_stride - pl.leaf_words < 4
+    assert pl.leaf_stride % 4 == 0 and (pl.leaf_stride // 4) % 2 == 1
+    assert pl.leaf_stride - pl.leaf_words < 8
 
 
 def test_plan_errors(lib):
