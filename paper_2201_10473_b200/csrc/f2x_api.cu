@@ -222,7 +222,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         }
         const int KC = std::min(K, kMaxKC);
         if (!find_k2(int(LF), KC)) continue;
-        const double cost = double(ipow3(K)) * double(LF * LF + 16 * LF);
+        // leaf LOP3 (LF^2 per leaf) + per-leaf Karatsuba/tree overhead, which
+        // measured on B200 is worth ~48 LOP3 per leaf word (tools/quick_time)
+        const double cost = double(ipow3(K)) * double(LF * LF + 48 * LF);
         if (!bestLF || cost < best) {
             best = cost;
             bestLF = int(LF);
