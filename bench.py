@@ -45,6 +45,14 @@ def w_alg(t: int, cyclic: bool = True) -> float:
     return 144.0 * t ** math.log2(3) + (4.0 * t if cyclic else 0.0)
 
 
+def shard_rows(rank: int, world: int, per_gpu: int) -> slice:
+    """Rank r owns rows [per_gpu*r, per_gpu*(r+1)) of the seeded global batch
+    (weak scaling; independent products, no data-path collective)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank outside [0, world)")
+    return slice(rank * per_gpu, (rank + 1) * per_gpu)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,8 +222,8 @@ def gpu_arm(args) -> None:
     t = (n + 63) // 64
     # one seeded global batch; this rank's contiguous shard
     A_all, B_all = make_cyclic_inputs(n, bpg * world)
-    A = A_all[rank * bpg:(rank + 1) * bpg]
-    B = B_all[rank * bpg:(rank + 1) * bpg]
+    A = A_all[shard_rows(rank, world, bpg)]
+    B = B_all[shard_rows(rank, world, bpg)]
     dA = torch.from_numpy(np.ascontiguousarray(A).view(np.int64)).to(dev)
     dB = torch.from_numpy(np.ascontiguousarray(B).view(np.int64)).to(dev)
     dC = torch.empty_like(dA)
