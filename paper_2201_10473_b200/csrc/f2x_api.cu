@@ -408,33 +408,22 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         cudaStreamSynchronize(stream);
         cudaMemcpy(h.data(), kp.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         cudaFree(kp.prof);
-        double acc[7] = {0};
-        long long t0 = h[0], t1 = h[6];
-        for (int64_t b = 0; b < pl.node_ctas; ++b)
-            for (int i = 0; i < 6; ++i) acc[i] += double(h[b * 8 + i + 1] - h[b * 8 + i]);
         FILE *f = fopen(prof_path, "a");
-        if (f && h[7] < 0) {  // warp-specialised kernel: per-CTA accumulated cycles
-            double a[5] = {0};
+        if (f) {  // persistent kernels: per-CTA accumulated cycles, slot 7 = -nodes
+            double a[6] = {0};
             long long nodes = 0;
             int rows = 0;
             for (int64_t b = 0; b < pl.node_ctas && h[b * 8 + 7] < 0; ++b, ++rows) {
-                for (int i = 0; i < 5; ++i) a[i] += double(h[b * 8 + i]);
+                for (int i = 0; i < 6; ++i) a[i] += double(h[b * 8 + i]);
                 nodes += -h[b * 8 + 7];
             }
-            fprintf(f, "WS LF=%d ctas=%d nodes=%lld per node: tree load+eval %.0f, tree wait %.0f, tree interp+store %.0f | leaf wait %.0f, leaves %.0f\n",
-                    pl.leaf_words, rows, nodes, a[0] / nodes, a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes);
-            fclose(f);
-            f = nullptr;
-        }
-        if (f) {
-            fprintf(f, "LF=%d KC=%d GL=%d ctas=%lld avg cycles: setup %.0f load %.0f eval %.0f leaf %.0f interp %.0f store %.0f (first cta total %lld)\n",
-                    pl.leaf_words, pl.cta_levels, pl.global_levels, (long long)pl.node_ctas,
-                    acc[0] / pl.node_ctas, acc[1] / pl.node_ctas, acc[2] / pl.node_ctas,
-                    acc[3] / pl.node_ctas, acc[4] / pl.node_ctas, acc[5] / pl.node_ctas, t1 - t0);
+            if (nodes < 1) nodes = 1;
+            fprintf(f, "LF=%d KC=%d GL=%d ctas=%d nodes=%lld cycles/node per slot: %.0f %.0f %.0f %.0f %.0f %.0f  (classic: setup load eval leaf interp store | ws: tree-LE tree-wait tree-IS leaf-wait leaves)\n",
+                    pl.leaf_words, pl.cta_levels, pl.global_levels, rows, nodes, a[0] / nodes,
+                    a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes, a[5] / nodes);
             fclose(f);
         }
     }
-    if ((rc = debug_sync(stream, 2))) return rc;
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
     int d = pl.global_levels;
