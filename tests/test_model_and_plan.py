@@ -155,3 +155,33 @@ def test_workspace_query(lib):
     b = lib.f2x_workspace_bytes(1, 8192, 17669, 0)
     assert 0 < a < b
     assert lib.f2x_workspace_bytes(1, 4096, 17669, 18) > 0
+
+
+def _pos_chunks_port(KC, j, nu):
+    """Line-by-line port of the kernel's pos_chunks<KC>(j, nu)."""
+    digs, v = 0, nu
+    for l in range(j):
+        digs |= (v % 3) << (2 * l)
+        v //= 3
+    pos = prefix = 0
+    p3 = 1
+    for l in range(j):
+        d = (digs >> (2 * (j - 1 - l))) & 3
+        h = 1 << (KC - l - 1)
+        R = (1 << (KC - l)) * p3
+        pos = pos if d == 0 else (pos + h if d == 1 else R + prefix * h)
+        prefix = prefix * 3 + d
+        p3 *= 3
+    return pos
+
+
+def test_arithmetic_positions_match_table():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "gen", os.path.join(ROOT, "paper_2201_10473_b200", "csrc", "gen_instances.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    for KC in range(1, 6):
+        flat = [_pos_chunks_port(KC, j, nu) for j in range(KC + 1) for nu in range(3 ** j)]
+        assert flat == gen.pos_table(KC)
