@@ -51,15 +51,29 @@ static inline int64_t ipow3(int k) {
 }
 
 // ------------------------------------------------------------------- K1
-// One thread = one (group, operand word u): 32 rows x 64 coefficients.
+// Warp w of a block owns operand words u in [u0, u0+32) of one group: lane l
+// loads word u0+l of the group's 32 rows (coalesced across lanes), transposes
+// the two 32x32 bit blocks in registers, parks its 64 coefficient words in a
+// padded shared stage (row stride 65: conflict-free), and the warp then
+// writes the contiguous storage range of coefficients [64 u0, 64 (u0+32)) in
+// the chunked layout, pads included (coalesced 128-byte stores).
+constexpr int kStage = 65;
+
+__device__ __forceinline__ void chunk_split(int k, int LF, int &c, int &r) {
+    c = k / LF;
+    r = k - c * LF;
+}
+
 __global__ void __launch_bounds__(kThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
          uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
-         int ncyc, uint32_t *d_err, int UB, int64_t items) {
-    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (item >= items) return;
-    const int64_t g = item / UB;
-    const int u = int(item - g * UB);
+         int ncyc, uint32_t *d_err, int UB, int tiles) {
+    __shared__ uint32_t stage[kThreads / 32][32 * kStage];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g = blockIdx.x / tiles;
+    const int u0 = int(blockIdx.x - g * tiles) * kThreads + warp * 32;
+    if (u0 >= UB) return;  // warp-uniform
+    const int u = u0 + lane;
     const uint64_t *X = blockIdx.y ? B : A;
     uint32_t *out = (blockIdx.y ? Bbs : Abs) + g * Ns;
 
@@ -79,22 +93,32 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
         atomicOr(d_err, uint32_t((bad | (bad >> 32)) != 0));
     transpose32(lo);
     transpose32(hi);
-
-    // coefficient k = 64u + i -> storage (k / LF) * LFS + k % LF
-    const int k0 = 64 * u;
-    int c = k0 / LF, r = k0 - c * LF;
+    uint32_t *st = stage[warp];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-        if (k0 + i < N) out[int64_t(c) * LFS + r] = i < 32 ? lo[i] : hi[i - 32];
-        if (++r == LF) {
-            r = 0;
+    for (int i = 0; i < 32; ++i) {
+        st[lane * kStage + i] = lo[i];
+        st[lane * kStage + 32 + i] = hi[i];
+    }
+    __syncwarp();
+    const int k0 = 64 * u0, k1 = min(64 * (u0 + 32), N);
+    int c, r;
+    chunk_split(k0, LF, c, r);
+    const int s0 = c * LFS + r;
+    chunk_split(k1, LF, c, r);
+    const int s1 = c * LFS + r;  // k1 on a chunk boundary => previous chunk's pads included
+    chunk_split(s0 + lane, LFS, c, r);  // storage word -> (chunk, offset)
+    for (int sw = s0 + lane; sw < s1; sw += 32) {
+        uint32_t v = 0u;
+        if (r < LF) {
+            const int k = c * LF + r - k0;
+            v = st[(k >> 6) * kStage + (k & 63)];
+        }
+        out[sw] = v;
+        r += 32;
+        while (r >= LFS) {
+            r -= LFS;
             ++c;
         }
-    }
-    // zero the pad words of every chunk that starts inside [k0, k0 + 64)
-    if (LFS > LF) {
-        for (int cc = (k0 + LF - 1) / LF; cc * LF < min(k0 + 64, N); ++cc)
-            for (int rr = LF; rr < LFS; ++rr) out[int64_t(cc) * LFS + rr] = 0u;
     }
 }
 
@@ -142,44 +166,67 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
 }
 
 // ------------------------------------------------------------------- K4
-// One thread = one (group, output word u): fold (cyclic), transpose, store.
+// Warp w of a block owns output words u in [u0, u0+32) of one group: the warp
+// gathers coefficients [64 u0, 64 (u0+32)) of the root product from the
+// chunked layout with coalesced loads (and, for the ring, XORs in the
+// coefficients k+n -- the fold mod X^n - 1 -- and zeroes k >= n), parks them
+// in a padded shared stage, then lane l transposes its 64 words back to 32
+// rows and stores word u0+l of each row (coalesced across lanes).
 __global__ void __launch_bounds__(kThreads)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
-           int LF, int LFS, int64_t rootStride, int ncyc, int64_t items) {
-    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (item >= items) return;
-    const int64_t g = item / tout;
-    const int u = int(item - g * tout);
+           int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
+    __shared__ uint32_t stage[kThreads / 32][32 * kStage];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g = blockIdx.x / tiles;
+    const int u0 = int(blockIdx.x - g * tiles) * kThreads + warp * 32;
+    if (u0 >= tout) return;  // warp-uniform
     const uint32_t *Cg = Croot + g * rootStride;
-
+    uint32_t *st = stage[warp];
+    const int k0 = 64 * u0, kend = 64 * min(u0 + 32, tout);
+    const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
+    {
+        int c, r;
+        chunk_split(k0 + lane, LF, c, r);
+        for (int k = k0 + lane; k < kend; k += 32) {
+            const uint32_t v = k < kvalid ? __ldg(Cg + int64_t(c) * LFS + r) : 0u;
+            const int kk = k - k0;
+            st[(kk >> 6) * kStage + (kk & 63)] = v;
+            r += 32;
+            while (r >= LF) {
+                r -= LF;
+                ++c;
+            }
+        }
+    }
+    if (ncyc > 0) {  // fold: coefficient k += coefficient k + n
+        int c, r;
+        chunk_split(k0 + lane + ncyc, LF, c, r);
+        for (int k = k0 + lane; k < kvalid; k += 32) {
+            const int kk = k - k0;
+            st[(kk >> 6) * kStage + (kk & 63)] ^= __ldg(Cg + int64_t(c) * LFS + r);
+            r += 32;
+            while (r >= LF) {
+                r -= LF;
+                ++c;
+            }
+        }
+    }
+    __syncwarp();
     uint32_t lo[32], hi[32];
-    const int k0 = 64 * u;
-    int c = k0 / LF, r = k0 - c * LF;
-    if (ncyc > 0) {
-        const int k1 = k0 + ncyc;
-        int c2 = k1 / LF, r2 = k1 - c2 * LF;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-            uint32_t v = 0u;
-            if (k0 + i < ncyc) v = __ldg(Cg + int64_t(c) * LFS + r) ^ __ldg(Cg + int64_t(c2) * LFS + r2);
-            if (i < 32) lo[i] = v; else hi[i - 32] = v;
-            if (++r == LF) { r = 0; ++c; }
-            if (++r2 == LF) { r2 = 0; ++c2; }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-            const uint32_t v = __ldg(Cg + int64_t(c) * LFS + r);
-            if (i < 32) lo[i] = v; else hi[i - 32] = v;
-            if (++r == LF) { r = 0; ++c; }
-        }
+    for (int i = 0; i < 32; ++i) {
+        lo[i] = st[lane * kStage + i];
+        hi[i] = st[lane * kStage + 32 + i];
     }
     transpose32(lo);
     transpose32(hi);
+    const int u = u0 + lane;
+    if (u < tout) {
 #pragma unroll
-    for (int pr = 0; pr < 32; ++pr) {
-        const int64_t row = g * 32 + pr;
-        if (row < batch) out[row * tout + u] = uint64_t(lo[pr]) | (uint64_t(hi[pr]) << 32);
+        for (int pr = 0; pr < 32; ++pr) {
+            const int64_t row = g * 32 + pr;
+            if (row < batch) out[row * tout + u] = uint64_t(lo[pr]) | (uint64_t(hi[pr]) << 32);
+        }
     }
 }
 
@@ -377,10 +424,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // K1
     const int UB = int(ceil_div(pl.N, 64));
     {
-        const int64_t items = G * UB;
-        dim3 grid(unsigned(ceil_div(items, kThreads)), 2);
+        const int tiles = int(ceil_div(UB, kThreads));
+        dim3 grid(unsigned(G * tiles), 2);
         k1_slice<<<grid, kThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N, pl.leaf_words,
-                                                pl.leaf_stride, L.Ns, ncyc, d_err, UB, items);
+                                                pl.leaf_stride, L.Ns, ncyc, d_err, UB, tiles);
     }
     if ((rc = debug_sync(stream, 1))) return rc;
     // K2
@@ -453,9 +500,9 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // K4
     {
         const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
-        const int64_t items = G * tout;
-        k4_unslice<<<unsigned(ceil_div(items, kThreads)), kThreads, 0, stream>>>(
-            cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, items);
+        const int tiles = int(ceil_div(tout, kThreads));
+        k4_unslice<<<unsigned(G * tiles), kThreads, 0, stream>>>(
+            cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, tiles);
     }
     if ((rc = debug_sync(stream, 4))) return rc;
     const cudaError_t ce = cudaGetLastError();
