@@ -172,7 +172,7 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
 // coefficients k+n -- the fold mod X^n - 1 -- and zeroes k >= n), parks them
 // in a padded shared stage, then lane l transposes its 64 words back to 32
 // rows and stores word u0+l of each row (coalesced across lanes).
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
     __shared__ uint32_t stage[kThreads / 32][32 * kStage];
@@ -184,31 +184,37 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     uint32_t *st = stage[warp];
     const int k0 = 64 * u0, kend = 64 * min(u0 + 32, tout);
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
-    {
-        int c, r;
-        chunk_split(k0 + lane, LF, c, r);
-        for (int k = k0 + lane; k < kend; k += 32) {
-            const uint32_t v = k < kvalid ? __ldg(Cg + int64_t(c) * LFS + r) : 0u;
-            const int kk = k - k0;
-            st[(kk >> 6) * kStage + (kk & 63)] = v;
+    // lane l gathers coefficients k0 + l + 32 m, m < 64, in two rounds of 32
+    // independent loads issued back to back.  (c, r) advance by 32
+    // coefficients per step: at most two chunk wraps since LF >= 16.
+    int c, r, c2 = 0, r2 = 0;
+    chunk_split(k0 + lane, LF, c, r);
+    if (ncyc > 0) chunk_split(k0 + lane + ncyc, LF, c2, r2);
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        uint32_t v[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            const int k = k0 + lane + 32 * (32 * half + m);
+            v[m] = k < kvalid ? __ldg(Cg + int64_t(c) * LFS + r) : 0u;
             r += 32;
-            while (r >= LF) {
-                r -= LF;
-                ++c;
+            if (r >= LF) { r -= LF; ++c; }
+            if (r >= LF) { r -= LF; ++c; }
+        }
+        if (ncyc > 0) {  // fold: coefficient k ^= coefficient k + n
+#pragma unroll
+            for (int m = 0; m < 32; ++m) {
+                const int k = k0 + lane + 32 * (32 * half + m);
+                if (k < kvalid) v[m] ^= __ldg(Cg + int64_t(c2) * LFS + r2);
+                r2 += 32;
+                if (r2 >= LF) { r2 -= LF; ++c2; }
+                if (r2 >= LF) { r2 -= LF; ++c2; }
             }
         }
-    }
-    if (ncyc > 0) {  // fold: coefficient k += coefficient k + n
-        int c, r;
-        chunk_split(k0 + lane + ncyc, LF, c, r);
-        for (int k = k0 + lane; k < kvalid; k += 32) {
-            const int kk = k - k0;
-            st[(kk >> 6) * kStage + (kk & 63)] ^= __ldg(Cg + int64_t(c) * LFS + r);
-            r += 32;
-            while (r >= LF) {
-                r -= LF;
-                ++c;
-            }
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            const int kk = lane + 32 * (32 * half + m);  // < 2048
+            st[(kk >> 6) * kStage + (kk & 63)] = v[m];
         }
     }
     __syncwarp();
