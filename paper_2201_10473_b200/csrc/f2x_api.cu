@@ -50,75 +50,77 @@ static inline int64_t ipow3(int k) {
     return r;
 }
 
-// ------------------------------------------------------------------- K1
-// Warp w of a block owns operand words u in [u0, u0+32) of one group: lane l
-// loads word u0+l of the group's 32 rows (coalesced across lanes), transposes
-// the two 32x32 bit blocks in registers, parks its 64 coefficient words in a
-// padded shared stage (row stride 65: conflict-free), and the warp then
-// writes the contiguous storage range of coefficients [64 u0, 64 (u0+32)) in
-// the chunked layout, pads included (coalesced 128-byte stores).
-constexpr int kStage = 65;
+// ------------------------------------------------------------------- K1/K4
+// Both memory-side kernels work on a TILE of 64 operand words (4096
+// coefficients) of one group with 128 threads: thread i owns half-word i
+// (32 coefficients) of the tile and does one 32x32 bit transpose in
+// registers; the chunked bitsliced side goes through a shared stage and is
+// read/written as a contiguous run of storage words by all 128 threads
+// (coalesced, pads included).  Storage word -> (chunk, offset) uses a float
+// reciprocal with one correction step (indices < 2^24).
+constexpr int kTileWords = 64;                 // uint64 operand words per tile
+constexpr int kTileCoeffs = 64 * kTileWords;   // 4096
+constexpr int kTileThreads = 2 * kTileWords;   // one 32x32 transpose each
 
 __device__ __forceinline__ void chunk_split(int k, int LF, int &c, int &r) {
     c = k / LF;
     r = k - c * LF;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void divmod_f(int s, int d, float inv, int &c, int &r) {
+    c = int(float(s) * inv);
+    r = s - c * d;
+    if (r < 0) { r += d; --c; }
+    if (r >= d) { r -= d; ++c; }
+}
+
+// half-word stage index with one pad word per 32 (conflict-free transposes)
+__device__ __forceinline__ int stg(int k) { return k + (k >> 5); }
+
+__global__ void __launch_bounds__(kTileThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
          uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
-         int ncyc, uint32_t *d_err, int UB, int tiles) {
-    __shared__ uint32_t stage[kThreads / 32][32 * kStage];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+         int ncyc, uint32_t *d_err, int tiles) {
+    __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
+    const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
-    const int u0 = int(blockIdx.x - g * tiles) * kThreads + warp * 32;
-    if (u0 >= UB) return;  // warp-uniform
-    const int u = u0 + lane;
-    const uint64_t *X = blockIdx.y ? B : A;
+    const int tile = int(blockIdx.x - g * tiles);
+    const int u = tile * kTileWords + (tid >> 1);  // operand word of this half-word
+    const int half = tid & 1;
+    const uint32_t *X = reinterpret_cast<const uint32_t *>(blockIdx.y ? B : A);
     uint32_t *out = (blockIdx.y ? Bbs : Abs) + g * Ns;
 
-    uint32_t lo[32], hi[32];
-    uint64_t bad = 0;
-    const uint64_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u < 64)
-                                ? (~0ull << (ncyc - 64 * u)) : 0ull;
+    // load: 32 rows x one 32-bit half-word (adjacent threads = adjacent halves)
+    uint32_t x[32];
+    uint32_t bad = 0;
+    const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
+                                ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
+                                : 0u;
 #pragma unroll
     for (int pr = 0; pr < 32; ++pr) {
         const int64_t row = g * 32 + pr;
-        const uint64_t v = (row < batch && u < t) ? __ldg(X + row * t + u) : 0ull;
+        const uint32_t v = (row < batch && u < t) ? __ldg(X + (row * t + u) * 2 + half) : 0u;
         bad |= v & himask;
-        lo[pr] = uint32_t(v);
-        hi[pr] = uint32_t(v >> 32);
+        x[pr] = v;
     }
     if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
-        atomicOr(d_err, uint32_t((bad | (bad >> 32)) != 0));
-    transpose32(lo);
-    transpose32(hi);
-    uint32_t *st = stage[warp];
+        atomicOr(d_err, uint32_t(bad != 0));
+    transpose32(x);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        st[lane * kStage + i] = lo[i];
-        st[lane * kStage + 32 + i] = hi[i];
-    }
-    __syncwarp();
-    const int k0 = 64 * u0, k1 = min(64 * (u0 + 32), N);
+    for (int i = 0; i < 32; ++i) stage[stg(32 * tid + i)] = x[i];
+    __syncthreads();
+    // store the contiguous storage range of coefficients [k0, k1)
+    const int k0 = tile * kTileCoeffs, k1 = min(k0 + kTileCoeffs, N);
+    if (k0 >= k1) return;
     int c, r;
     chunk_split(k0, LF, c, r);
     const int s0 = c * LFS + r;
     chunk_split(k1, LF, c, r);
     const int s1 = c * LFS + r;  // k1 on a chunk boundary => previous chunk's pads included
-    chunk_split(s0 + lane, LFS, c, r);  // storage word -> (chunk, offset)
-    for (int sw = s0 + lane; sw < s1; sw += 32) {
-        uint32_t v = 0u;
-        if (r < LF) {
-            const int k = c * LF + r - k0;
-            v = st[(k >> 6) * kStage + (k & 63)];
-        }
-        out[sw] = v;
-        r += 32;
-        while (r >= LFS) {
-            r -= LFS;
-            ++c;
-        }
+    const float inv = 1.0f / float(LFS);
+    for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+        divmod_f(sw, LFS, inv, c, r);
+        out[sw] = r < LF ? stage[stg(c * LF + r - k0)] : 0u;
     }
 }
 
@@ -165,73 +167,59 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
     for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qw] = v[m];
 }
 
-// ------------------------------------------------------------------- K4
-// Warp w of a block owns output words u in [u0, u0+32) of one group: the warp
-// gathers coefficients [64 u0, 64 (u0+32)) of the root product from the
-// chunked layout with coalesced loads (and, for the ring, XORs in the
-// coefficients k+n -- the fold mod X^n - 1 -- and zeroes k >= n), parks them
-// in a padded shared stage, then lane l transposes its 64 words back to 32
-// rows and stores word u0+l of each row (coalesced across lanes).
-__global__ void __launch_bounds__(kThreads, 4)
+// K4: the tile's 4096 coefficients of the root product are gathered (and,
+// for the ring, folded: c[k] ^= c[k+n]; k >= n zero) into the
+// stage from contiguous storage runs, then thread i transposes half-word i
+// back to 32 rows and stores its 32-bit halves (adjacent threads = adjacent
+// halves of a row: coalesced).
+__global__ void __launch_bounds__(kTileThreads)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
-    __shared__ uint32_t stage[kThreads / 32][32 * kStage];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
+    const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
-    const int u0 = int(blockIdx.x - g * tiles) * kThreads + warp * 32;
-    if (u0 >= tout) return;  // warp-uniform
+    const int tile = int(blockIdx.x - g * tiles);
     const uint32_t *Cg = Croot + g * rootStride;
-    uint32_t *st = stage[warp];
-    const int k0 = 64 * u0, kend = 64 * min(u0 + 32, tout);
+    const int k0 = tile * kTileCoeffs, kend = min(k0 + kTileCoeffs, 64 * tout);
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
-    // lane l gathers coefficients k0 + l + 32 m, m < 64, in two rounds of 32
-    // independent loads issued back to back.  (c, r) advance by 32
-    // coefficients per step: at most two chunk wraps since LF >= 16.
-    int c, r, c2 = 0, r2 = 0;
-    chunk_split(k0 + lane, LF, c, r);
-    if (ncyc > 0) chunk_split(k0 + lane + ncyc, LF, c2, r2);
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-        uint32_t v[32];
-#pragma unroll
-        for (int m = 0; m < 32; ++m) {
-            const int k = k0 + lane + 32 * (32 * half + m);
-            v[m] = k < kvalid ? __ldg(Cg + int64_t(c) * LFS + r) : 0u;
-            r += 32;
-            if (r >= LF) { r -= LF; ++c; }
-            if (r >= LF) { r -= LF; ++c; }
-        }
-        if (ncyc > 0) {  // fold: coefficient k ^= coefficient k + n
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
-                const int k = k0 + lane + 32 * (32 * half + m);
-                if (k < kvalid) v[m] ^= __ldg(Cg + int64_t(c2) * LFS + r2);
-                r2 += 32;
-                if (r2 >= LF) { r2 -= LF; ++c2; }
-                if (r2 >= LF) { r2 -= LF; ++c2; }
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < 32; ++m) {
-            const int kk = lane + 32 * (32 * half + m);  // < 2048
-            st[(kk >> 6) * kStage + (kk & 63)] = v[m];
+    const float inv = 1.0f / float(LFS);
+    for (int k = k0 + tid; k < k0 + kTileCoeffs; k += kTileThreads)
+        if (k >= kvalid) stage[stg(k - k0)] = 0u;
+    int c, r;
+    if (k0 < kvalid) {
+        chunk_split(k0, LF, c, r);
+        const int s0 = c * LFS + r;
+        chunk_split(kvalid, LF, c, r);
+        const int s1 = c * LFS + r;
+        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+            divmod_f(sw, LFS, inv, c, r);
+            if (r < LF) stage[stg(c * LF + r - k0)] = __ldg(Cg + sw);
         }
     }
-    __syncwarp();
-    uint32_t lo[32], hi[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        lo[i] = st[lane * kStage + i];
-        hi[i] = st[lane * kStage + 32 + i];
+    __syncthreads();
+    if (ncyc > 0 && k0 < kvalid) {  // fold: coefficients [k0+n, kvalid+n)
+        chunk_split(k0 + ncyc, LF, c, r);
+        const int s0 = c * LFS + r;
+        chunk_split(kvalid + ncyc, LF, c, r);
+        const int s1 = c * LFS + r;
+        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+            divmod_f(sw, LFS, inv, c, r);
+            if (r < LF) stage[stg(c * LF + r - ncyc - k0)] ^= __ldg(Cg + sw);
+        }
+        __syncthreads();
     }
-    transpose32(lo);
-    transpose32(hi);
-    const int u = u0 + lane;
+    uint32_t x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = stage[stg(32 * tid + i)];
+    transpose32(x);
+    const int u = tile * kTileWords + (tid >> 1);
     if (u < tout) {
+        uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
+        const int half = tid & 1;
 #pragma unroll
         for (int pr = 0; pr < 32; ++pr) {
             const int64_t row = g * 32 + pr;
-            if (row < batch) out[row * tout + u] = uint64_t(lo[pr]) | (uint64_t(hi[pr]) << 32);
+            if (row < batch) o32[(row * tout + u) * 2 + half] = x[pr];
         }
     }
 }
@@ -428,12 +416,12 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     const int ncyc = kind == F2X_KIND_CYCLIC ? pl.n : 0;
 
     // K1
-    const int UB = int(ceil_div(pl.N, 64));
     {
-        const int tiles = int(ceil_div(UB, kThreads));
+        const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
-        k1_slice<<<grid, kThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N, pl.leaf_words,
-                                                pl.leaf_stride, L.Ns, ncyc, d_err, UB, tiles);
+        k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+                                                    pl.leaf_words, pl.leaf_stride, L.Ns, ncyc,
+                                                    d_err, tiles);
     }
     if ((rc = debug_sync(stream, 1))) return rc;
     // K2
@@ -506,8 +494,8 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // K4
     {
         const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
-        const int tiles = int(ceil_div(tout, kThreads));
-        k4_unslice<<<unsigned(G * tiles), kThreads, 0, stream>>>(
+        const int tiles = int(ceil_div(tout, kTileWords));
+        k4_unslice<<<unsigned(G * tiles), kTileThreads, 0, stream>>>(
             cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, tiles);
     }
     if ((rc = debug_sync(stream, 4))) return rc;
