@@ -53,6 +53,23 @@ def shard_rows(rank: int, world: int, per_gpu: int) -> slice:
     return slice(rank * per_gpu, (rank + 1) * per_gpu)
 
 
+def committed_traffic(pl) -> dict | None:
+    """DRAM bytes per node-kernel launch from the latest committed ncu --set
+    full capture (profiles/r*/k2_traffic.json) for this workload, else None."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k2_traffic.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if d.get("workload") == "n=17669 x4096" and pl.get("leaf_words") == 35:
+            best = {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"],
+                    "algorithmic_bytes_per_launch": None}
+    return best
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -342,7 +359,7 @@ def gpu_arm(args) -> None:
                 "peak": round(pk, 3),
                 "unit": "T int32-lane-op/s",
                 "frac": round(achieved / pk, 4),
-                "traffic": None,
+                "traffic": committed_traffic(pl),
                 "work_per_product": round(W, 1),
                 "work_model": "W_alg = 144 t^log2(3) + 4t (SURVEY §8(d)), t=ceil(n/64)",
                 "peak_source": "live LOP3 microbenchmark (c^(a&b), 8 chains/thread, 8 CTAs/SM) this run",
