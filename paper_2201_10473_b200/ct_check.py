@@ -1,0 +1,111 @@
+"""Statistical constant-time check (SPEC ``ct_check``).
+
+Fixed-vs-random timing test: a weight-w sparse first operand (the HQC secret
+shape) against a dense random first operand, interleaved
+trials, Welch's t statistic on the per-call times; |t| < 4.5 passes.  On the
+GPU every call is timed with CUDA events around one ring product of a batch
+of 32 (one bitsliced group).  ``leaky_mul`` is the positive control the SPEC
+asks for: a sparse convolution that only visits the set bits of A (its time
+grows with the weight), which must fail.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+THRESHOLD = 4.5
+
+
+def welch_t(x, y) -> float:
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    vx, vy = x.var(ddof=1) / x.size, y.var(ddof=1) / y.size
+    if vx + vy == 0:
+        return 0.0
+    return float((x.mean() - y.mean()) / math.sqrt(vx + vy))
+
+
+def _sparse_rows(n: int, weight: int, rows: int, rng) -> np.ndarray:
+    from .ring import sparse_to_dense
+
+    return np.stack([sparse_to_dense(rng.choice(n, weight, replace=False), n).words
+                     for _ in range(rows)])
+
+
+def _dense_rows(n: int, rows: int, rng) -> np.ndarray:
+    t = (n + 63) // 64
+    A = rng.integers(0, 1 << 64, size=(rows, t), dtype=np.uint64)
+    r = n - 64 * (t - 1)
+    if r < 64:
+        A[:, -1] &= np.uint64((1 << r) - 1)
+    return A
+
+
+def ct_check(n: int = 17669, weight: int = 75, trials: int = 2000, seed: int = 0xC7,
+             batch: int = 32) -> dict:
+    """GPU fixed(sparse)-vs-random(dense) timing test of ``mul_cyclic``."""
+    import torch
+
+    from .engine import mul_cyclic
+
+    rng = np.random.default_rng(seed)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    B = torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev)
+    sparse = torch.from_numpy(_sparse_rows(n, weight, batch, rng).view(np.int64)).to(dev)
+    pool = [torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev) for _ in range(8)]
+    out = torch.empty_like(B)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    for _ in range(10):
+        mul_cyclic(sparse, B, n, out=out, check=False, err_flag=flag)
+    torch.cuda.synchronize()
+    t_fix, t_rnd = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    order = rng.integers(0, 2, size=2 * trials)
+    for i, cls in enumerate(order):
+        A = sparse if cls == 0 else pool[i % len(pool)]
+        e0.record()
+        mul_cyclic(A, B, n, out=out, check=False, err_flag=flag)
+        e1.record()
+        e1.synchronize()
+        (t_fix if cls == 0 else t_rnd).append(e0.elapsed_time(e1))
+    t = welch_t(t_fix, t_rnd)
+    return {"n": n, "weight": weight, "trials": [len(t_fix), len(t_rnd)],
+            "mean_ms": [float(np.mean(t_fix)), float(np.mean(t_rnd))], "t": t,
+            "verdict": "pass" if abs(t) < THRESHOLD else "fail"}
+
+
+def leaky_mul(a: int, b: int, n: int) -> int:
+    """Deliberately leaky ring product: loops over the set bits of a only."""
+    r = 0
+    mask = (1 << n) - 1
+    while a:
+        low = a & -a
+        i = low.bit_length() - 1
+        r ^= ((b << i) | (b >> (n - i))) & mask if i else b
+        a ^= low
+    return r
+
+
+def ct_check_leaky(n: int = 2000, weight: int = 20, trials: int = 300, seed: int = 0xC8) -> dict:
+    """Positive control on the CPU: the leaky multiplier must FAIL."""
+    rng = np.random.default_rng(seed)
+    b = int.from_bytes(rng.bytes((n + 7) // 8), "little") & ((1 << n) - 1)
+    sparse = sum(1 << int(i) for i in rng.choice(n, weight, replace=False))
+    t_fix, t_rnd = [], []
+    for cls in rng.integers(0, 2, size=2 * trials):
+        a = sparse if cls == 0 else int.from_bytes(rng.bytes((n + 7) // 8), "little") & ((1 << n) - 1)
+        t0 = time.perf_counter()
+        leaky_mul(a, b, n)
+        (t_fix if cls == 0 else t_rnd).append(time.perf_counter() - t0)
+    t = welch_t(t_fix, t_rnd)
+    return {"n": n, "weight": weight, "t": t, "verdict": "pass" if abs(t) < THRESHOLD else "fail"}
+
+
+if __name__ == "__main__":
+    import json
+
+    print(json.dumps(ct_check()))
+    print(json.dumps(ct_check_leaky()))
