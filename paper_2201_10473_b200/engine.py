@@ -134,3 +134,73 @@ def clmul64_lanes(a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, torch
         return a.clone(), a.clone()
     lohi = mul_full(a.reshape(-1, 1).contiguous(), b.reshape(-1, 1).contiguous())
     return lohi[:, 0], lohi[:, 1]
+
+
+class HostPipeline:
+    """Products of HOST-resident operands (pinned torch tensors), end to end.
+
+    The batch is cut into ``chunks`` row blocks issued round-robin on
+    ``streams`` CUDA streams, each with its own device buffers: H2D of chunk
+    i+1, the engine on chunk i and D2H of chunk i-1 overlap (copy engines
+    and SMs work concurrently).  ``run`` enqueues one whole batch behind the
+    current stream and makes the current stream wait for it, so callers time
+    it with ordinary events.  ``kind`` is "cyclic" (size = n) or "full"
+    (size = t words).
+    """
+
+    def __init__(self, kind: str, size: int, batch: int, device=None, chunks: int = 4,
+                 streams: int = 3, leaf: int = 0):
+        if kind not in ("cyclic", "full"):
+            raise ValueError("kind must be 'cyclic' or 'full'")
+        self.kind, self.size, self.batch, self.leaf = kind, int(size), int(batch), leaf
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.t = (self.size + 63) // 64 if kind == "cyclic" else self.size
+        self.tout = self.t if kind == "cyclic" else 2 * self.t
+        chunks = max(1, min(chunks, batch))
+        step = -(-batch // chunks)
+        step = -(-step // 32) * 32  # whole bitsliced groups per chunk
+        self.bounds = [(i, min(i + step, batch)) for i in range(0, batch, step)]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(max(1, streams))]
+        rows = self.bounds[0][1] - self.bounds[0][0]
+        self.bufs = []
+        for _ in self.streams:
+            self.bufs.append((torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
+                              torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
+                              torch.empty((rows, self.tout), dtype=torch.int64, device=self.device),
+                              torch.zeros(1, dtype=torch.int32, device=self.device)))
+
+    def run(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> torch.Tensor:
+        """hA, hB: pinned [batch, t] word tensors; hC: pinned [batch, tout]."""
+        if hA.shape != (self.batch, self.t) or hB.shape != hA.shape or \
+                hC.shape != (self.batch, self.tout):
+            raise ValueError("host buffers do not match the pipeline shape")
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            s.wait_stream(cur)
+        for i, (lo, hi) in enumerate(self.bounds):
+            k = i % len(self.streams)
+            s = self.streams[k]
+            dA, dB, dC, flag = self.bufs[k]
+            r = hi - lo
+            with torch.cuda.stream(s):
+                dA[:r].copy_(hA[lo:hi], non_blocking=True)
+                dB[:r].copy_(hB[lo:hi], non_blocking=True)
+                if self.kind == "cyclic":
+                    mul_cyclic(dA[:r], dB[:r], self.size, out=dC[:r], leaf=self.leaf,
+                               check=False, err_flag=flag)
+                else:
+                    mul_full(dA[:r], dB[:r], out=dC[:r], leaf=self.leaf)
+                hC[lo:hi].copy_(dC[:r], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        return hC
+
+    def rejected(self) -> bool:
+        """True if any ring operand since the last reset had a bit >= n."""
+        torch.cuda.synchronize(self.device)
+        return any(int(b[3].item()) != 0 for b in self.bufs)
+
+    def reset_flags(self) -> None:
+        for b in self.bufs:
+            b[3].zero_()

@@ -246,3 +246,29 @@ def test_ring_weight75_dense_path(cuda):
     _, B = make_cyclic_inputs(n, 32)
     out = mul_cyclic(_dev(A, cuda), _dev(B, cuda), n)
     assert np.array_equal(_np(out), c_mul_cyclic(A, B, n))
+
+
+@pytest.mark.parametrize("kind,size,batch,chunks", [("cyclic", 17669, 300, 4), ("full", 64, 100, 3),
+                                                     ("cyclic", 1000, 31, 2)])
+def test_host_pipeline(kind, size, batch, chunks, cuda):
+    """Pinned-host end-to-end path (chunked over streams) == oracle."""
+    import torch
+
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200.engine import HostPipeline
+
+    if kind == "cyclic":
+        A, B = make_cyclic_inputs(size, batch)
+        want = c_mul_cyclic(A, B, size)
+    else:
+        A, B = make_full_inputs(size, batch, words=True)
+        want = c_mul_full(A, B)
+    hA = torch.from_numpy(A.view(np.int64)).pin_memory()
+    hB = torch.from_numpy(B.view(np.int64)).pin_memory()
+    hC = torch.empty((batch, want.shape[1]), dtype=torch.int64).pin_memory()
+    pipe = HostPipeline(kind, size, batch, cuda, chunks=chunks)
+    pipe.run(hA, hB, hC)
+    torch.cuda.synchronize()
+    assert not pipe.rejected()
+    assert np.array_equal(hC.numpy().view(np.uint64), want)
