@@ -296,6 +296,8 @@ def gpu_arm(args) -> None:
     hC = torch.empty_like(hA).pin_memory()
     pipe = HostPipeline("cyclic", n, bpg, dev, chunks=args.e2e_chunks, streams=3, leaf=args.leaf)
 
+    graphed = pipe.capture(hA, hB, hC) if not args.no_graph else False
+
     def e2e_step():
         pipe.run(hA, hB, hC)
 
@@ -379,7 +381,8 @@ def gpu_arm(args) -> None:
                 "d2h_bytes_per_step": int(bpg * t * 8),
                 "ms_per_step": round(e2e_ms, 5),
                 "path": f"pinned host A,B -> H2D -> mul_cyclic (C ABI) -> D2H; engine.HostPipeline, "
-                        f"{args.e2e_chunks} chunks over 3 streams (copies overlap compute)",
+                        f"{args.e2e_chunks} chunks over 3 streams (copies overlap compute)"
+                        + (", replayed as one CUDA graph" if graphed else ", eager launches"),
             },
             "gpu_launches": int(K * pl["launches"]),
             "clocks": cl,
@@ -473,6 +476,7 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--leaf", type=int, default=0)
     ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
     ap.add_argument("--quick", action="store_true", help="skip the extra-config lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     args = ap.parse_args()

@@ -163,6 +163,7 @@ class HostPipeline:
         self.bounds = [(i, min(i + step, batch)) for i in range(0, batch, step)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(max(1, streams))]
         rows = self.bounds[0][1] - self.bounds[0][0]
+        self.graph, self.graph_key = None, None
         self.bufs = []
         for _ in self.streams:
             self.bufs.append((torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
@@ -171,10 +172,36 @@ class HostPipeline:
                               torch.zeros(1, dtype=torch.int32, device=self.device)))
 
     def run(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> torch.Tensor:
-        """hA, hB: pinned [batch, t] word tensors; hC: pinned [batch, tout]."""
+        """hA, hB: pinned [batch, t] word tensors; hC: pinned [batch, tout].
+        Replays the captured CUDA graph when these exact buffers were captured."""
         if hA.shape != (self.batch, self.t) or hB.shape != hA.shape or \
                 hC.shape != (self.batch, self.tout):
             raise ValueError("host buffers do not match the pipeline shape")
+        if self.graph is not None and self.graph_key == (hA.data_ptr(), hB.data_ptr(),
+                                                         hC.data_ptr()):
+            self.graph.replay()
+            return hC
+        self._enqueue(hA, hB, hC)
+        return hC
+
+    def capture(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> bool:
+        """Capture one whole batch (copies + every engine launch on every
+        stream) into a CUDA graph bound to these host buffers: later ``run``
+        calls on them cost one graph launch of CPU time.  Returns False (and
+        stays eager) if capture is not possible."""
+        self.run(hA, hB, hC)  # warm: workspaces and buffers exist before capture
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                self._enqueue(hA, hB, hC)
+        except Exception:
+            self.graph = None
+            return False
+        self.graph, self.graph_key = g, (hA.data_ptr(), hB.data_ptr(), hC.data_ptr())
+        return True
+
+    def _enqueue(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> None:
         cur = torch.cuda.current_stream(self.device)
         for s in self.streams:
             s.wait_stream(cur)
@@ -194,7 +221,6 @@ class HostPipeline:
                 hC[lo:hi].copy_(dC[:r], non_blocking=True)
         for s in self.streams:
             cur.wait_stream(s)
-        return hC
 
     def rejected(self) -> bool:
         """True if any ring operand since the last reset had a bit >= n."""

@@ -272,3 +272,27 @@ def test_host_pipeline(kind, size, batch, chunks, cuda):
     torch.cuda.synchronize()
     assert not pipe.rejected()
     assert np.array_equal(hC.numpy().view(np.uint64), want)
+
+
+def test_host_pipeline_graph_replay(cuda):
+    """The captured CUDA graph of the host path gives the oracle's answer on
+    fresh data written into the same pinned buffers."""
+    import torch
+
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200.engine import HostPipeline
+
+    n, batch = 17669, 256
+    A, B = make_cyclic_inputs(n, batch)
+    hA = torch.from_numpy(A.view(np.int64).copy()).pin_memory()
+    hB = torch.from_numpy(B.view(np.int64).copy()).pin_memory()
+    hC = torch.empty_like(hA).pin_memory()
+    pipe = HostPipeline("cyclic", n, batch, cuda, chunks=4)
+    assert pipe.capture(hA, hB, hC)
+    A2, B2 = np.roll(A, 3, axis=0), np.roll(B, 5, axis=0)
+    hA.copy_(torch.from_numpy(A2.view(np.int64)))
+    hB.copy_(torch.from_numpy(B2.view(np.int64)))
+    pipe.run(hA, hB, hC)
+    torch.cuda.synchronize()
+    assert np.array_equal(hC.numpy().view(np.uint64), c_mul_cyclic(A2, B2, n))
