@@ -139,17 +139,19 @@ def clmul64_lanes(a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, torch
 class HostPipeline:
     """Products of HOST-resident operands (pinned torch tensors), end to end.
 
-    The batch is cut into ``chunks`` row blocks issued round-robin on
+    A batch is cut into ``chunks`` row blocks issued round-robin on
     ``streams`` CUDA streams, each with its own device buffers: H2D of chunk
-    i+1, the engine on chunk i and D2H of chunk i-1 overlap (copy engines
-    and SMs work concurrently).  ``run`` enqueues one whole batch behind the
-    current stream and makes the current stream wait for it, so callers time
-    it with ordinary events.  ``kind`` is "cyclic" (size = n) or "full"
+    i+1, the engine on chunk i and D2H of chunk i-1 overlap (copy engines and
+    SMs work concurrently).  ``lanes`` independent copies of those buffers and
+    streams let consecutive batches overlap too (batch j+1's first upload runs
+    under batch j's last chunks): ``run(..., lane=j % lanes)``.  ``capture``
+    records a lane's batch as one CUDA graph; ``join`` makes the current
+    stream wait for every lane.  ``kind`` is "cyclic" (size = n) or "full"
     (size = t words).
     """
 
     def __init__(self, kind: str, size: int, batch: int, device=None, chunks: int = 4,
-                 streams: int = 3, leaf: int = 0):
+                 streams: int = 3, leaf: int = 0, lanes: int = 1):
         if kind not in ("cyclic", "full"):
             raise ValueError("kind must be 'cyclic' or 'full'")
         self.kind, self.size, self.batch, self.leaf = kind, int(size), int(batch), leaf
@@ -161,54 +163,70 @@ class HostPipeline:
         step = -(-batch // chunks)
         step = -(-step // 32) * 32  # whole bitsliced groups per chunk
         self.bounds = [(i, min(i + step, batch)) for i in range(0, batch, step)]
-        self.streams = [torch.cuda.Stream(self.device) for _ in range(max(1, streams))]
         rows = self.bounds[0][1] - self.bounds[0][0]
-        self.graph, self.graph_key = None, None
-        self.bufs = []
-        for _ in self.streams:
-            self.bufs.append((torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
-                              torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
-                              torch.empty((rows, self.tout), dtype=torch.int64, device=self.device),
-                              torch.zeros(1, dtype=torch.int32, device=self.device)))
+        self.lanes = []
+        for _ in range(max(1, lanes)):
+            streams = [torch.cuda.Stream(self.device) for _ in range(max(1, streams))]
+            bufs = [(torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
+                     torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
+                     torch.empty((rows, self.tout), dtype=torch.int64, device=self.device),
+                     torch.zeros(1, dtype=torch.int32, device=self.device)) for _ in streams]
+            self.lanes.append({"launch": torch.cuda.Stream(self.device), "streams": streams,
+                               "bufs": bufs, "graph": None, "key": None})
 
-    def run(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> torch.Tensor:
-        """hA, hB: pinned [batch, t] word tensors; hC: pinned [batch, tout].
-        Replays the captured CUDA graph when these exact buffers were captured."""
+    def _check(self, hA, hB, hC):
         if hA.shape != (self.batch, self.t) or hB.shape != hA.shape or \
                 hC.shape != (self.batch, self.tout):
             raise ValueError("host buffers do not match the pipeline shape")
-        if self.graph is not None and self.graph_key == (hA.data_ptr(), hB.data_ptr(),
-                                                         hC.data_ptr()):
-            self.graph.replay()
-            return hC
-        self._enqueue(hA, hB, hC)
+
+    def run(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor, lane: int = 0
+            ) -> torch.Tensor:
+        """Enqueue one batch on ``lane`` (after the work already queued on the
+        current stream).  hA, hB: pinned [batch, t]; hC: pinned [batch, tout].
+        Replays the lane's CUDA graph when it was captured on these buffers."""
+        self._check(hA, hB, hC)
+        L = self.lanes[lane % len(self.lanes)]
+        L["launch"].wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(L["launch"]):
+            if L["graph"] is not None and L["key"] == (hA.data_ptr(), hB.data_ptr(),
+                                                       hC.data_ptr()):
+                L["graph"].replay()
+            else:
+                self._enqueue(L, hA, hB, hC)
         return hC
 
-    def capture(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> bool:
-        """Capture one whole batch (copies + every engine launch on every
-        stream) into a CUDA graph bound to these host buffers: later ``run``
-        calls on them cost one graph launch of CPU time.  Returns False (and
-        stays eager) if capture is not possible."""
-        self.run(hA, hB, hC)  # warm: workspaces and buffers exist before capture
+    def join(self) -> None:
+        cur = torch.cuda.current_stream(self.device)
+        for L in self.lanes:
+            cur.wait_stream(L["launch"])
+
+    def capture(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor, lane: int = 0
+                ) -> bool:
+        """Capture one whole batch of ``lane`` (copies + every engine launch on
+        every stream) as a CUDA graph bound to these host buffers: later
+        ``run`` calls on them cost one graph launch of CPU time.  Returns
+        False (and stays eager) if capture is not possible."""
+        L = self.lanes[lane % len(self.lanes)]
+        self.run(hA, hB, hC, lane)  # warm: workspaces and buffers exist before capture
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         try:
             with torch.cuda.graph(g):
-                self._enqueue(hA, hB, hC)
+                self._enqueue(L, hA, hB, hC)
         except Exception:
-            self.graph = None
+            L["graph"] = None
             return False
-        self.graph, self.graph_key = g, (hA.data_ptr(), hB.data_ptr(), hC.data_ptr())
+        L["graph"], L["key"] = g, (hA.data_ptr(), hB.data_ptr(), hC.data_ptr())
         return True
 
-    def _enqueue(self, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> None:
+    def _enqueue(self, L, hA: torch.Tensor, hB: torch.Tensor, hC: torch.Tensor) -> None:
         cur = torch.cuda.current_stream(self.device)
-        for s in self.streams:
+        for s in L["streams"]:
             s.wait_stream(cur)
         for i, (lo, hi) in enumerate(self.bounds):
-            k = i % len(self.streams)
-            s = self.streams[k]
-            dA, dB, dC, flag = self.bufs[k]
+            k = i % len(L["streams"])
+            s = L["streams"][k]
+            dA, dB, dC, flag = L["bufs"][k]
             r = hi - lo
             with torch.cuda.stream(s):
                 dA[:r].copy_(hA[lo:hi], non_blocking=True)
@@ -219,14 +237,15 @@ class HostPipeline:
                 else:
                     mul_full(dA[:r], dB[:r], out=dC[:r], leaf=self.leaf)
                 hC[lo:hi].copy_(dC[:r], non_blocking=True)
-        for s in self.streams:
+        for s in L["streams"]:
             cur.wait_stream(s)
 
     def rejected(self) -> bool:
         """True if any ring operand since the last reset had a bit >= n."""
         torch.cuda.synchronize(self.device)
-        return any(int(b[3].item()) != 0 for b in self.bufs)
+        return any(int(b[3].item()) != 0 for L in self.lanes for b in L["bufs"])
 
     def reset_flags(self) -> None:
-        for b in self.bufs:
-            b[3].zero_()
+        for L in self.lanes:
+            for b in L["bufs"]:
+                b[3].zero_()

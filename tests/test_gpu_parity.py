@@ -267,8 +267,9 @@ def test_host_pipeline(kind, size, batch, chunks, cuda):
     hA = torch.from_numpy(A.view(np.int64)).pin_memory()
     hB = torch.from_numpy(B.view(np.int64)).pin_memory()
     hC = torch.empty((batch, want.shape[1]), dtype=torch.int64).pin_memory()
-    pipe = HostPipeline(kind, size, batch, cuda, chunks=chunks)
-    pipe.run(hA, hB, hC)
+    pipe = HostPipeline(kind, size, batch, cuda, chunks=chunks, lanes=2)
+    pipe.run(hA, hB, hC, lane=1)
+    pipe.join()
     torch.cuda.synchronize()
     assert not pipe.rejected()
     assert np.array_equal(hC.numpy().view(np.uint64), want)
