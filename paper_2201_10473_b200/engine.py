@@ -165,13 +165,14 @@ class HostPipeline:
         self.bounds = [(i, min(i + step, batch)) for i in range(0, batch, step)]
         rows = self.bounds[0][1] - self.bounds[0][0]
         self.lanes = []
+        nstreams = max(1, int(streams))
         for _ in range(max(1, lanes)):
-            streams = [torch.cuda.Stream(self.device) for _ in range(max(1, streams))]
+            ss = [torch.cuda.Stream(self.device) for _ in range(nstreams)]
             bufs = [(torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
                      torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
                      torch.empty((rows, self.tout), dtype=torch.int64, device=self.device),
-                     torch.zeros(1, dtype=torch.int32, device=self.device)) for _ in streams]
-            self.lanes.append({"launch": torch.cuda.Stream(self.device), "streams": streams,
+                     torch.zeros(1, dtype=torch.int32, device=self.device)) for _ in ss]
+            self.lanes.append({"launch": torch.cuda.Stream(self.device), "streams": ss,
                                "bufs": bufs, "graph": None, "key": None})
 
     def _check(self, hA, hB, hC):
