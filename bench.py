@@ -488,7 +488,7 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=N_RING)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--leaf", type=int, default=0)
-    ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--e2e-chunks", type=int, default=2)
     ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
     ap.add_argument("--quick", action="store_true", help="skip the extra-config lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
