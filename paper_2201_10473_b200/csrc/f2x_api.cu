@@ -39,7 +39,7 @@ static const K2Entry *find_k2(int LF, int KC) {
 
 static constexpr int kMaxKC = 5;
 static constexpr int kMaxGL = 8;
-static constexpr int kMaxPassLevels = 3;
+static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -118,6 +118,7 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     chunk_split(k1, LF, c, r);
     const int s1 = c * LFS + r;  // k1 on a chunk boundary => previous chunk's pads included
     const float inv = 1.0f / float(LFS);
+#pragma unroll 8
     for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
         divmod_f(sw, LFS, inv, c, r);
         out[sw] = r < LF ? stage[stg(c * LF + r - k0)] : 0u;
@@ -191,7 +192,8 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid, LF, c, r);
         const int s1 = c * LFS + r;
-        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+    #pragma unroll 8
+    for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
             divmod_f(sw, LFS, inv, c, r);
             if (r < LF) stage[stg(c * LF + r - k0)] = __ldg(Cg + sw);
         }
@@ -202,7 +204,8 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid + ncyc, LF, c, r);
         const int s1 = c * LFS + r;
-        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+    #pragma unroll 8
+    for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
             divmod_f(sw, LFS, inv, c, r);
             if (r < LF) stage[stg(c * LF + r - ncyc - k0)] ^= __ldg(Cg + sw);
         }
@@ -478,6 +481,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             case 1: launch_k3<1>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             case 2: launch_k3<2>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             case 3: launch_k3<3>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
+            case 4: launch_k3<4>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             default: return F2X_ERANGE;
         }
         if (getenv("F2X_DEBUG_SYNC"))

@@ -219,7 +219,7 @@ def k4(plan: Plan, C: np.ndarray) -> np.ndarray:
     return out
 
 
-def split_passes(GL: int, maxp: int = 3):
+def split_passes(GL: int, maxp: int = 4):
     passes = []
     rem = GL
     while rem > 0:
