@@ -453,7 +453,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         cudaMemcpy(h.data(), kp.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
         cudaFree(kp.prof);
         FILE *f = fopen(prof_path, "a");
-        if (f) {  // persistent kernels: per-CTA accumulated cycles, slot 7 = -nodes
+        if (f) {  // per-CTA phase cycles (one node per CTA), slot 7 = -nodes
             double a[6] = {0};
             long long nodes = 0;
             int rows = 0;
@@ -462,7 +462,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                 nodes += -h[b * 8 + 7];
             }
             if (nodes < 1) nodes = 1;
-            fprintf(f, "LF=%d KC=%d GL=%d ctas=%d nodes=%lld cycles/node per slot: %.0f %.0f %.0f %.0f %.0f %.0f  (classic: setup load eval leaf interp store | ws: tree-LE tree-wait tree-IS leaf-wait leaves)\n",
+            fprintf(f, "LF=%d KC=%d GL=%d ctas=%d nodes=%lld cycles/node per slot: %.0f %.0f %.0f %.0f %.0f %.0f  (setup load eval leaf interp store)\n",
                     pl.leaf_words, pl.cta_levels, pl.global_levels, rows, nodes, a[0] / nodes,
                     a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes, a[5] / nodes);
             fclose(f);

@@ -158,7 +158,8 @@ def test_workspace_query(lib):
 
 
 def _pos_chunks_port(KC, j, nu):
-    """Line-by-line port of the kernel's pos_chunks<KC>(j, nu)."""
+    """Digit-walk derivation of pos_j(nu) (top-down, MS digit first), an
+    independent construction of the kernels' kPosChunks table."""
     digs, v = 0, nu
     for l in range(j):
         digs |= (v % 3) << (2 * l)
