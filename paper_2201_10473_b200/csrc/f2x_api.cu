@@ -56,8 +56,7 @@ static inline int64_t ipow3(int k) {
 // (32 coefficients) of the tile and does one 32x32 bit transpose in
 // registers; the chunked bitsliced side goes through a shared stage and is
 // read/written as a contiguous run of storage words by all 128 threads
-// (coalesced, pads included).  Storage word -> (chunk, offset) uses a float
-// reciprocal with one correction step (indices < 2^24).
+// (coalesced, pads included), walked incrementally (StorageWalk).
 constexpr int kTileWords = 64;                 // uint64 operand words per tile
 constexpr int kTileCoeffs = 64 * kTileWords;   // 4096
 constexpr int kTileThreads = 2 * kTileWords;   // one 32x32 transpose each
@@ -67,15 +66,32 @@ __device__ __forceinline__ void chunk_split(int k, int LF, int &c, int &r) {
     r = k - c * LF;
 }
 
-__device__ __forceinline__ void divmod_f(int s, int d, float inv, int &c, int &r) {
-    c = int(float(s) * inv);
-    r = s - c * d;
-    if (r < 0) { r += d; --c; }
-    if (r >= d) { r -= d; ++c; }
-}
-
 // half-word stage index with one pad word per 32 (conflict-free transposes)
 __device__ __forceinline__ int stg(int k) { return k + (k >> 5); }
+
+// Walk storage words sw = s0 + tid, s0 + tid + 128, ... < s1 of the chunked
+// layout, tracking r = sw mod LFS and the coefficient index kk = chunk*LF + r
+// (relative to kbase) incrementally: one divmod per thread, then adds.
+struct StorageWalk {
+    int r, kk, dr, dkk, LF, LFS;
+    __device__ __forceinline__ StorageWalk(int sw, int kbase, int LF_, int LFS_) : LF(LF_), LFS(LFS_) {
+        const int c = sw / LFS;
+        r = sw - c * LFS;
+        kk = c * LF + r - kbase;
+        const int dc = kTileThreads / LFS;
+        dr = kTileThreads - dc * LFS;
+        dkk = dc * LF + dr;
+    }
+    __device__ __forceinline__ bool data() const { return r < LF; }
+    __device__ __forceinline__ void next() {
+        r += dr;
+        kk += dkk;
+        if (r >= LFS) {
+            r -= LFS;
+            kk += LF - LFS;
+        }
+    }
+};
 
 __global__ void __launch_bounds__(kTileThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
@@ -96,10 +112,12 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
                                 ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
                                 : 0u;
+    const int rows = u < t ? int(min<int64_t>(32, batch - g * 32)) : 0;
+    const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
 #pragma unroll
     for (int pr = 0; pr < 32; ++pr) {
-        const int64_t row = g * 32 + pr;
-        const uint32_t v = (row < batch && u < t) ? __ldg(X + (row * t + u) * 2 + half) : 0u;
+        const uint32_t v = pr < rows ? __ldg(px) : 0u;
+        px += 2 * int64_t(t);
         bad |= v & himask;
         x[pr] = v;
     }
@@ -117,11 +135,11 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     const int s0 = c * LFS + r;
     chunk_split(k1, LF, c, r);
     const int s1 = c * LFS + r;  // k1 on a chunk boundary => previous chunk's pads included
-    const float inv = 1.0f / float(LFS);
-#pragma unroll 8
+    StorageWalk w(s0 + tid, k0, LF, LFS);
+#pragma unroll 4
     for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
-        divmod_f(sw, LFS, inv, c, r);
-        out[sw] = r < LF ? stage[stg(c * LF + r - k0)] : 0u;
+        out[sw] = w.data() ? stage[stg(w.kk)] : 0u;
+        w.next();
     }
 }
 
@@ -183,7 +201,6 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     const uint32_t *Cg = Croot + g * rootStride;
     const int k0 = tile * kTileCoeffs, kend = min(k0 + kTileCoeffs, 64 * tout);
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
-    const float inv = 1.0f / float(LFS);
     for (int k = k0 + tid; k < k0 + kTileCoeffs; k += kTileThreads)
         if (k >= kvalid) stage[stg(k - k0)] = 0u;
     int c, r;
@@ -192,10 +209,11 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid, LF, c, r);
         const int s1 = c * LFS + r;
-    #pragma unroll 8
-    for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
-            divmod_f(sw, LFS, inv, c, r);
-            if (r < LF) stage[stg(c * LF + r - k0)] = __ldg(Cg + sw);
+        StorageWalk w(s0 + tid, k0, LF, LFS);
+#pragma unroll 4
+        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+            if (w.data()) stage[stg(w.kk)] = __ldg(Cg + sw);
+            w.next();
         }
     }
     __syncthreads();
@@ -204,10 +222,11 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid + ncyc, LF, c, r);
         const int s1 = c * LFS + r;
-    #pragma unroll 8
-    for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
-            divmod_f(sw, LFS, inv, c, r);
-            if (r < LF) stage[stg(c * LF + r - ncyc - k0)] ^= __ldg(Cg + sw);
+        StorageWalk w(s0 + tid, k0 + ncyc, LF, LFS);
+#pragma unroll 4
+        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+            if (w.data()) stage[stg(w.kk)] ^= __ldg(Cg + sw);
+            w.next();
         }
         __syncthreads();
     }
@@ -217,12 +236,12 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     transpose32(x);
     const int u = tile * kTileWords + (tid >> 1);
     if (u < tout) {
-        uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
-        const int half = tid & 1;
+        const int rows = int(min<int64_t>(32, batch - g * 32));
+        uint32_t *po = reinterpret_cast<uint32_t *>(out) + ((g * 32) * tout + u) * 2 + (tid & 1);
 #pragma unroll
         for (int pr = 0; pr < 32; ++pr) {
-            const int64_t row = g * 32 + pr;
-            if (row < batch) o32[(row * tout + u) * 2 + half] = x[pr];
+            if (pr < rows) *po = x[pr];
+            po += 2 * int64_t(tout);
         }
     }
 }
