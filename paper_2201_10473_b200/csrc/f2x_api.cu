@@ -112,7 +112,7 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
                                 ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
                                 : 0u;
-    const int rows = u < t ? int(min<int64_t>(32, batch - g * 32)) : 0;
+    const int rows = u < t ? int(batch - g * 32 < 32 ? batch - g * 32 : 32) : 0;
     const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
 #pragma unroll
     for (int pr = 0; pr < 32; ++pr) {
@@ -236,7 +236,7 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     transpose32(x);
     const int u = tile * kTileWords + (tid >> 1);
     if (u < tout) {
-        const int rows = int(min<int64_t>(32, batch - g * 32));
+        const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
         uint32_t *po = reinterpret_cast<uint32_t *>(out) + ((g * 32) * tout + u) * 2 + (tid & 1);
 #pragma unroll
         for (int pr = 0; pr < 32; ++pr) {
