@@ -175,7 +175,11 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t items, int qw,
           int64_t inStride, int64_t outStride) {
-    const int64_t item = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // blocks walk the nodes in REVERSE order: the node kernel wrote them in
+    // forward order, so the most recently written (still L2-resident)
+    // products are consumed first instead of being evicted by the rest
+    const int64_t nblk = (items + blockDim.x - 1) / blockDim.x;
+    const int64_t item = (nblk - 1 - int64_t(blockIdx.x)) * blockDim.x + threadIdx.x;
     if (item >= items) return;
     const int64_t node = item / qw;
     const int w = int(item - node * qw);
