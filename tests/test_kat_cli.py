@@ -69,3 +69,14 @@ def test_cli_mul_gpu(tmp_path):
     assert r.stdout.strip() == "0" * 16 + "0000000000000001"  # 1*1 = 1, 2t words
     r = _run_cli("mul", str(tmp_path / "a"), str(tmp_path / "b"), "--ring", "100")
     assert r.returncode == 0 and r.stdout.strip() == "0" * 16 + "0000000000000001"
+
+
+@pytest.mark.gpu
+def test_cli_bench_gpu():
+    import json
+
+    r = _run_cli("bench", "--sizes", "1000", "--batch", "64", "--datasets", "2", "--runs", "3",
+                 "--format", "json")
+    assert r.returncode == 0, r.stderr
+    rows = json.loads(r.stdout)
+    assert rows[0]["size_bits"] == 1000 and rows[0]["products_per_s"] > 0

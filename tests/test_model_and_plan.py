@@ -186,3 +186,20 @@ def test_arithmetic_positions_match_table():
     for KC in range(1, 6):
         flat = [_pos_chunks_port(KC, j, nu) for j in range(KC + 1) for nu in range(3 ** j)]
         assert flat == gen.pos_table(KC)
+
+
+@pytest.mark.parametrize("kind,size", [(1, 17669), (1, 35851), (1, 57637), (0, 16), (0, 1024)])
+def test_plan_counts_match_closed_forms(lib, kind, size):
+    """Counter conservation (Table 1): the plan's analytic counts
+    follow the KaratRec closed forms -- 3^K leaf products of LF x LF
+    coefficients (LF^2/32 LOP3 each per product, bitsliced over 32), and
+    eval+interp XOR work sum_j 3^j * 5 * LF*2^(K-j-1) / 32 per product."""
+    from paper_2201_10473_b200 import _lib
+
+    pl = _lib.make_plan(kind, 4096, size)
+    LF, K = pl.leaf_words, pl.levels
+    assert pl.leaf_ops_per_product == pytest.approx(3 ** K * LF * LF / 32)
+    xors = sum(3 ** j * 5 * (LF << (K - j - 1)) for j in range(K)) / 32
+    assert pl.karatsuba_ops_per_product == pytest.approx(xors)
+    # KaratRec base-multiplication count for 2^K leaves is 3^K (Table 1, t^log2(3))
+    assert round((2 ** K) ** np.log2(3)) == 3 ** K
