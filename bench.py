@@ -53,6 +53,32 @@ def shard_rows(rank: int, world: int, per_gpu: int) -> slice:
     return slice(rank * per_gpu, (rank + 1) * per_gpu)
 
 
+def committed_ncu(pl) -> dict | None:
+    """Pipe utilisation / DRAM figures of the node kernel from the latest
+    committed ncu --set full capture for this workload."""
+    import csv
+    import glob
+
+    out = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k2_node_mul_raw.csv"))):
+        try:
+            rows = list(csv.reader(open(f)))
+            d = dict(zip(rows[0], rows[2]))
+            dur_s = float(d["gpu__time_duration.sum"]) * 1e-6
+            dram = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * 1e6
+            out = {
+                "source": os.path.relpath(f, ROOT),
+                "pipe_alu_pct": float(d["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"]),
+                "pipe_fma_pct": float(d["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"]),
+                "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+                "dram_GBps": round(dram / dur_s / 1e9, 1),
+                "duration_us": float(d["gpu__time_duration.sum"]),
+            }
+        except Exception:
+            continue
+    return out if pl.get("leaf_words") == 35 else None
+
+
 def committed_traffic(pl) -> dict | None:
     """DRAM bytes per node-kernel launch from the latest committed ncu --set
     full capture (profiles/r*/k2_traffic.json) for this workload, else None."""
@@ -397,6 +423,13 @@ def gpu_arm(args) -> None:
                         + (", replayed as one CUDA graph" if graphed else ", eager launches")
                         + f"; {LANES} batches in flight (double-buffered pinned host buffers)",
             },
+            "plan_work": {
+                "leaf_lop3_per_product": round(pl["leaf_ops_per_product"], 1),
+                "karatsuba_xor_ops_per_product": round(pl["karatsuba_ops_per_product"], 1),
+                "base_mul_64x64_equiv_per_product": round(pl["leaf_ops_per_product"] / 128.0, 1),
+                "note": "analytic counts of the executed plan; W_alg charges 144 t^log2(3)",
+            },
+            "ncu_node_kernel": committed_ncu(pl),
             "gpu_launches": int(K * pl["launches"]),
             "clocks": cl,
         }
