@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
 from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+from paper_2201_10473_b200._lib import load
+lib = load()
 
 dev = torch.device("cuda", 0)
 cfgs = [("cyc", 12323, 256), ("cyc", 17669, 4096), ("cyc", 35851, 4096), ("cyc", 57637, 16384),
@@ -28,17 +30,23 @@ for kind, size, batch in cfgs:
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = 10
+    nv = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in nv:  # torch creates the cudaEvent_t lazily, on first record
+        a.record(); b.record()
     e0.record()
-    for _ in range(iters):
+    for i in range(iters):
+        lib.f2x_set_node_events(nv[i][0].cuda_event, nv[i][1].cuda_event)
         f()
     e1.record()
+    lib.f2x_set_node_events(None, None)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
+    node_ms = sum(a.elapsed_time(b) for a, b in nv) / iters
     p = plan("cyclic" if kind == "cyc" else "full", batch, size, leaf)
     t = p["t"]
     W = 144 * t ** np.log2(3) + (4 * t if kind == "cyc" else 0)
     pint = 148 * 64 * 1.965e9
-    print(json.dumps({"kind": kind, "size": size, "batch": batch, "ms": round(ms, 4),
+    print(json.dumps({"kind": kind, "size": size, "batch": batch, "ms": round(ms, 4), "node_ms": round(node_ms, 4),
                       "prod_per_s": round(batch / ms * 1e3), "frac_L64": round(batch / ms * 1e3 * W / pint, 3),
                       "LF": p["leaf_words"], "K": p["levels"], "GL": p["global_levels"],
                       "passes": p["pass_levels"], "ctas": p["node_ctas"], "ws_MB": p["workspace_bytes"] >> 20}))
