@@ -214,9 +214,10 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         chunk_split(kvalid, LF, c, r);
         const int s1 = c * LFS + r;
         StorageWalk w(s0 + tid, k0, LF, LFS);
-#pragma unroll 4
+#pragma unroll 8
         for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
-            if (w.data()) stage[stg(w.kk)] = __ldg(Cg + sw);
+            const uint32_t v = __ldg(Cg + sw);  // pads too: loads batch across the unroll
+            if (w.data()) stage[stg(w.kk)] = v;
             w.next();
         }
     }
@@ -227,9 +228,10 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         chunk_split(kvalid + ncyc, LF, c, r);
         const int s1 = c * LFS + r;
         StorageWalk w(s0 + tid, k0 + ncyc, LF, LFS);
-#pragma unroll 4
+#pragma unroll 8
         for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
-            if (w.data()) stage[stg(w.kk)] ^= __ldg(Cg + sw);
+            const uint32_t v = __ldg(Cg + sw);
+            if (w.data()) stage[stg(w.kk)] ^= v;
             w.next();
         }
         __syncthreads();

@@ -203,3 +203,19 @@ def test_plan_counts_match_closed_forms(lib, kind, size):
     assert pl.karatsuba_ops_per_product == pytest.approx(xors)
     # KaratRec base-multiplication count for 2^K leaves is 3^K (Table 1, t^log2(3))
     assert round((2 ** K) ** np.log2(3)) == 3 ** K
+
+
+def _byte_perm(x, y, sel):
+    b = [(x >> (8 * i)) & 255 for i in range(4)] + [(y >> (8 * i)) & 255 for i in range(4)]
+    return sum(b[(sel >> (4 * i)) & 7] << (8 * i) for i in range(4))
+
+
+def test_transpose_prmt_selectors():
+    """The byte-permute form of the 16/8-bit transpose stages
+    (f2x_kernels.cuh tstage_prmt) equals the masked-swap form."""
+    rng = np.random.default_rng(7)
+    for a, c in rng.integers(0, 1 << 32, size=(500, 2), dtype=np.uint64).tolist():
+        for J, m, sx, sy in ((16, 0x0000FFFF, 0x5410, 0x7632), (8, 0x00FF00FF, 0x6240, 0x7351)):
+            s = ((a >> J) ^ c) & m
+            assert _byte_perm(a, c, sx) == (a ^ (s << J)) & 0xFFFFFFFF
+            assert _byte_perm(a, c, sy) == c ^ s
