@@ -322,9 +322,11 @@ def gpu_arm(args) -> None:
     # ---- e2e: host pinned buffers, H2D + compute + D2H inside the timed region
     from paper_2201_10473_b200.engine import HostPipeline
 
-    # two host batches in flight (double-buffered pinned buffers, one pipeline
-    # lane each) so consecutive batches' copies overlap
-    LANES = 2
+    # several host batches in flight (one pinned buffer set and pipeline lane
+    # each) so batch j's H2D/D2H run under batch j-1's kernels; measured on
+    # the box (n=17669 x 4096): 1 chunk x 4 lanes 10.6 M/s, 2 x 2 9.7 M/s,
+    # 1 x 2 8.5 M/s (a whole-batch launch keeps the node grid at 23 waves)
+    LANES = max(1, args.e2e_lanes)
     hAs = [torch.from_numpy(np.ascontiguousarray(A).view(np.int64).copy()).pin_memory()
            for _ in range(LANES)]
     hBs = [torch.from_numpy(np.ascontiguousarray(B).view(np.int64).copy()).pin_memory()
@@ -424,9 +426,11 @@ def gpu_arm(args) -> None:
                 "d2h_bytes_per_step": int(bpg * t * 8),
                 "ms_per_step": round(e2e_ms, 5),
                 "path": f"pinned host A,B -> H2D -> mul_cyclic (C ABI) -> D2H; engine.HostPipeline, "
-                        f"{args.e2e_chunks} chunks over 3 streams (copies overlap compute)"
-                        + (", replayed as one CUDA graph" if graphed else ", eager launches")
-                        + f"; {LANES} batches in flight (double-buffered pinned host buffers)",
+                        f"{args.e2e_chunks} row chunk(s) per batch"
+                        + (", each batch replayed as one CUDA graph" if graphed else ", eager launches")
+                        + f"; {LANES} host batches in flight (one pinned buffer set per lane), so a "
+                        "batch's copies overlap the previous batches' kernels; pipeline fill and "
+                        "drain inside the timed region",
             },
             "plan_work": {
                 "leaf_lop3_per_product": round(pl["leaf_ops_per_product"], 1),
@@ -526,8 +530,11 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=N_RING)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--leaf", type=int, default=0)
-    ap.add_argument("--e2e-chunks", type=int, default=2)
+    ap.add_argument("--e2e-chunks", type=int, default=1,
+                    help="row chunks per host batch in the e2e pipeline")
     ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
+    ap.add_argument("--e2e-lanes", type=int, default=4,
+                    help="host batches in flight in the e2e pipeline (one pinned buffer set each)")
     ap.add_argument("--quick", action="store_true", help="skip the extra-config lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     args = ap.parse_args()
