@@ -73,6 +73,9 @@ typedef struct f2x_plan {
     int64_t workspace_bytes;
     double leaf_ops_per_product;    /* LOP3 in leaves / product (analytic)    */
     double karatsuba_ops_per_product; /* XOR ops of eval+interp / product     */
+    int32_t eval_levels;     /* top global levels pre-evaluated by the slicing
+                                kernel (node kernel runs on 3^eval_levels x
+                                the groups with levels - eval_levels)        */
 } f2x_plan;
 
 /* Fill *plan for a call shape.  leaf_hint = 0 picks the default leaf;

@@ -58,6 +58,7 @@ class F2xPlan(ctypes.Structure):
         ("workspace_bytes", ctypes.c_int64),
         ("leaf_ops_per_product", ctypes.c_double),
         ("karatsuba_ops_per_product", ctypes.c_double),
+        ("eval_levels", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

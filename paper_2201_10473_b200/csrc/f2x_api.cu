@@ -72,14 +72,15 @@ __device__ __forceinline__ int stg(int k) { return k + (k >> 5); }
 // Walk storage words sw = s0 + tid, s0 + tid + 128, ... < s1 of the chunked
 // layout, tracking r = sw mod LFS and the coefficient index kk = chunk*LF + r
 // (relative to kbase) incrementally: one divmod per thread, then adds.
-struct StorageWalk {
+template <int STEP>
+struct StorageWalkN {
     int r, kk, dr, dkk, LF, LFS;
-    __device__ __forceinline__ StorageWalk(int sw, int kbase, int LF_, int LFS_) : LF(LF_), LFS(LFS_) {
+    __device__ __forceinline__ StorageWalkN(int sw, int kbase, int LF_, int LFS_) : LF(LF_), LFS(LFS_) {
         const int c = sw / LFS;
         r = sw - c * LFS;
         kk = c * LF + r - kbase;
-        const int dc = kTileThreads / LFS;
-        dr = kTileThreads - dc * LFS;
+        const int dc = STEP / LFS;
+        dr = STEP - dc * LFS;
         dkk = dc * LF + dr;
     }
     __device__ __forceinline__ bool data() const { return r < LF; }
@@ -92,6 +93,7 @@ struct StorageWalk {
         }
     }
 };
+using StorageWalk = StorageWalkN<kTileThreads>;
 
 __global__ void __launch_bounds__(kTileThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
@@ -139,6 +141,86 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
 #pragma unroll 4
     for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
         out[sw] = w.data() ? stage[stg(w.kk)] : 0u;
+        w.next();
+    }
+}
+
+// K1 with the top EL global Karatsuba levels pre-evaluated (EL = 1, 2): the
+// CTA transposes the same tile of each of the 2^EL parts of the operand
+// (part j = coefficients [j N/2^EL, (j+1) N/2^EL)) into 2^EL stages, then
+// writes the 3^EL evaluated sub-operands (per level: lo, hi, lo^hi; top level
+// most significant -- the node numbering of the node kernel is unchanged; it
+// runs on 3^EL x the groups with K-EL levels and loads 2^EL x fewer segments
+// per mid path).
+template <int EL>
+__global__ void __launch_bounds__(kTileThreads << EL)
+k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
+              uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
+              int ncyc, uint32_t *d_err, int tiles) {
+    constexpr int NP = 1 << EL;               // parts
+    constexpr int NO = EL == 1 ? 3 : 9;       // evaluated sub-operands
+    constexpr int STG = kTileCoeffs + kTileCoeffs / 32;
+    extern __shared__ uint32_t stage[];       // [NP][STG]
+    const int tid = threadIdx.x & (kTileThreads - 1);
+    const int j = threadIdx.x / kTileThreads;  // part handled by this thread's 128-group
+    const int64_t g = blockIdx.x / tiles;
+    const int tile = int(blockIdx.x - g * tiles);
+    const int NE = N >> EL;                   // coefficients per part (multiple of 64)
+    const uint32_t *X = reinterpret_cast<const uint32_t *>(blockIdx.y ? B : A);
+    uint32_t *out = (blockIdx.y ? Eb : Ea) + g * (NO * NsE);
+    const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
+    const int half = tid & 1;
+    const int ul = tile * kTileWords + (tid >> 1);  // word within the part
+    {
+        const int u = j * (NE / 64) + ul;  // operand word
+        uint32_t x[32];
+        uint32_t bad = 0;
+        const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
+                                    ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
+                                    : 0u;
+        const int r = (u < t && ul < NE / 64) ? rows : 0;
+        const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            const uint32_t v = pr < r ? __ldg(px) : 0u;
+            px += 2 * int64_t(t);
+            bad |= v & himask;
+            x[pr] = v;
+        }
+        if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
+            atomicOr(d_err, uint32_t(bad != 0));
+        transpose32(x);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[j * STG + stg(32 * tid + i)] = x[i];
+    }
+    __syncthreads();
+    const int k0 = tile * kTileCoeffs, k1 = min(k0 + kTileCoeffs, NE);
+    if (k0 >= k1) return;
+    int c, r;
+    chunk_split(k0, LF, c, r);
+    const int s0 = c * LFS + r;
+    chunk_split(k1, LF, c, r);
+    const int s1 = c * LFS + r;
+    // all NP x 128 threads walk the storage range (stride NP x 128)
+    StorageWalkN<(kTileThreads << EL)> w(s0 + int(threadIdx.x), k0, LF, LFS);
+#pragma unroll 2
+    for (int sw = s0 + int(threadIdx.x); sw < s1; sw += kTileThreads << EL) {
+        uint32_t v[NP];
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) v[jj] = w.data() ? stage[jj * STG + stg(w.kk)] : 0u;
+        if constexpr (EL == 1) {
+            out[sw] = v[0];
+            out[NsE + sw] = v[1];
+            out[2 * NsE + sw] = v[0] ^ v[1];
+        } else {
+            const uint32_t h[3][2] = {{v[0], v[1]}, {v[2], v[3]}, {v[0] ^ v[2], v[1] ^ v[3]}};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                out[(3 * d) * NsE + sw] = h[d][0];
+                out[(3 * d + 1) * NsE + sw] = h[d][1];
+                out[(3 * d + 2) * NsE + sw] = h[d][0] ^ h[d][1];
+            }
+        }
         w.next();
     }
 }
@@ -256,7 +338,24 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
 struct Layout {
     int64_t Ns, Ss;
     int64_t off_abs, off_bbs, off_p0, off_p1, total;
+    int el;  // pre-evaluated top global levels (K1b)
 };
+
+// Top global levels pre-evaluated by the slicing kernel (k1_slice_eval):
+// 2 where the parts are whole operand words; F2X_EVAL_LEVELS=0/1/2 overrides
+// (experiments).
+static int eval_levels_for(int GL, int64_t N) {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("F2X_EVAL_LEVELS");
+        v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : -1;
+    }
+    // default 2: measured +1.3% (n=17669), +2.6% (35851), +1.8% (57637)
+    int el = v >= 0 ? v : 2;
+    if (el > GL) el = GL;
+    while (el > 0 && (N >> el) % 64 != 0) --el;  // parts must be whole operand words
+    return el;
+}
 
 static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
                      Layout *lay) {
@@ -345,9 +444,11 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.Ns = int64_t(LFS) << K;
     L.Ss = int64_t(LFS) << KC;
     const int64_t G = pl->groups;
+    L.el = eval_levels_for(GL, int64_t(LF) << K);
+    const int64_t opw = G * ipow3(L.el) * (L.Ns >> L.el);  // operand words (evaluated)
     L.off_abs = 0;
-    L.off_bbs = align256(L.off_abs + G * L.Ns * 4);
-    L.off_p0 = align256(L.off_bbs + G * L.Ns * 4);
+    L.off_bbs = align256(L.off_abs + opw * 4);
+    L.off_p0 = align256(L.off_bbs + opw * 4);
     const int64_t p0 = G * ipow3(GL) * 2 * L.Ss * 4;
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
@@ -366,6 +467,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         }
     }
     pl->workspace_bytes = L.total;
+    pl->eval_levels = L.el;
     if (lay) *lay = L;
     return F2X_OK;
 }
@@ -443,13 +545,36 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     const int64_t G = pl.groups;
     const int ncyc = kind == F2X_KIND_CYCLIC ? pl.n : 0;
 
-    // K1
-    {
+    // K1 (with the top L.el global levels pre-evaluated when L.el > 0)
+    if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
         k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                     pl.leaf_words, pl.leaf_stride, L.Ns, ncyc,
                                                     d_err, tiles);
+    } else {
+        const int tiles = int(ceil_div(pl.N >> L.el, kTileCoeffs));
+        dim3 grid(unsigned(G * tiles), 2);
+        const size_t sm = size_t(1 << L.el) * (kTileCoeffs + kTileCoeffs / 32) * 4;
+        static int attr_dev_mask[3] = {0, 0, 0};  // benign race: the attribute set is idempotent
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 31 && !(attr_dev_mask[L.el] & (1 << dev))) {
+            const cudaError_t ae = L.el == 1
+                ? cudaFuncSetAttribute(k1_slice_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))
+                : cudaFuncSetAttribute(k1_slice_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
+            attr_dev_mask[L.el] |= 1 << dev;
+        }
+        if (L.el == 1) {
+            k1_slice_eval<1><<<grid, kTileThreads << 1, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+                                                                 pl.leaf_words, pl.leaf_stride,
+                                                                 L.Ns >> 1, ncyc, d_err, tiles);
+        } else {
+            k1_slice_eval<2><<<grid, kTileThreads << 2, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+                                                                 pl.leaf_words, pl.leaf_stride,
+                                                                 L.Ns >> 2, ncyc, d_err, tiles);
+        }
     }
     if ((rc = debug_sync(stream, 1))) return rc;
     // K2
@@ -458,10 +583,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.Abs = Abs;
     kp.Bbs = Bbs;
     kp.Pout = P0;
-    kp.Ns = L.Ns;
-    kp.K = pl.levels;
-    kp.GL = pl.global_levels;
-    kp.paths = int(ipow3(pl.global_levels));
+    kp.Ns = L.Ns >> L.el;
+    kp.K = pl.levels - L.el;
+    kp.GL = pl.global_levels - L.el;
+    kp.paths = int(ipow3(pl.global_levels - L.el));
     kp.prof = nullptr;
     const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
     if (prof_path) {

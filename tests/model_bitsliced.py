@@ -370,3 +370,35 @@ def run_v2(plan: Plan, A: np.ndarray, B: np.ndarray) -> np.ndarray:
         P = k3_pass(plan, P, d, glp)
         d -= glp
     return k4(plan, P[:, 0, :])
+
+
+def k1_eval(plan: Plan, X: np.ndarray, el: int) -> np.ndarray:
+    """k1_slice_eval: the top ``el`` global levels pre-evaluated -> 3^el
+    sub-operands per group (digits lo, hi, mid; top level most significant)."""
+    Xs = k1(plan, X)                                   # [G][Ns]
+    subs = [Xs]
+    for _ in range(el):
+        nxt = []
+        for s in subs:
+            h = s.shape[1] // 2
+            lo, hi = s[:, :h], s[:, h:]
+            nxt += [lo, hi, lo ^ hi]
+        subs = nxt
+    return np.stack(subs, axis=1).reshape(plan.G * pow3(el), -1)
+
+
+def run_v3(plan: Plan, A: np.ndarray, B: np.ndarray, el: int) -> np.ndarray:
+    """run_v2 with the slicing kernel's pre-evaluation of ``el`` levels: the
+    node kernel sees 3^el x the groups with K - el levels; node numbering,
+    interpolation and unslicing are unchanged."""
+    import copy
+
+    sub = copy.copy(plan)
+    sub.K, sub.GL, sub.Ns, sub.G = plan.K - el, plan.GL - el, plan.Ns >> el, plan.G * pow3(el)
+    P = k2_v2(sub, k1_eval(plan, A, el), k1_eval(plan, B, el))
+    P = P.reshape(plan.G, pow3(plan.GL), -1)
+    d = plan.GL
+    for glp in split_passes(plan.GL):
+        P = k3_pass(plan, P, d, glp)
+        d -= glp
+    return k4(plan, P[:, 0, :])

@@ -297,3 +297,41 @@ def test_host_pipeline_graph_replay(cuda):
     pipe.run(hA, hB, hC)
     torch.cuda.synchronize()
     assert np.array_equal(hC.numpy().view(np.uint64), c_mul_cyclic(A2, B2, n))
+
+
+_EL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import c_mul_cyclic, c_mul_full
+from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+el = int(sys.argv[2])
+dev = torch.device("cuda", 0)
+d = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)
+for n, b in ((12323, 70), (17669, 64), (57637, 33)):
+    assert plan("cyclic", b, n)["eval_levels"] == el
+    A, B = make_cyclic_inputs(n, b)
+    out = mul_cyclic(d(A), d(B), n).cpu().numpy().view(np.uint64)
+    assert np.array_equal(out, c_mul_cyclic(A, B, n)), n
+for t in (64, 256, 1024):
+    A, B = make_full_inputs(t, 40, words=True)
+    out = mul_full(d(A), d(B)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(out, c_mul_full(A, B)), t
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("el", [0, 1])
+def test_eval_levels_override(el, cuda):
+    """The slicing kernel's pre-evaluated global levels (default 2) are a pure
+    schedule choice: 0 and 1 (F2X_EVAL_LEVELS, read once per process) give
+    the same bits."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, F2X_EVAL_LEVELS=str(el))
+    r = subprocess.run([sys.executable, "-c", _EL_SCRIPT, root, str(el)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

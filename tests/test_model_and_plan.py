@@ -47,6 +47,8 @@ def test_model_matches_oracle(kind, t, n, LF, K, KC, batch):
         ref = o.mul_cyclic(A, B, n)
     assert np.array_equal(mb.run(p, A, B), ref)
     assert np.array_equal(mb.run_v2(p, A, B), ref)  # the kernels' current schedule
+    for el in range(1, min(2, p.GL) + 1):  # slicing kernel pre-evaluates el levels
+        assert np.array_equal(mb.run_v3(p, A, B, el), ref), el
 
 
 def test_position_table_matches_generator():
@@ -219,3 +221,21 @@ def test_transpose_prmt_selectors():
             s = ((a >> J) ^ c) & m
             assert _byte_perm(a, c, sx) == (a ^ (s << J)) & 0xFFFFFFFF
             assert _byte_perm(a, c, sy) == c ^ s
+
+
+@pytest.mark.parametrize("kind,size", [("cyclic", 12323), ("cyclic", 17669), ("cyclic", 35851),
+                                       ("cyclic", 57637), ("full", 1), ("full", 16), ("full", 64),
+                                       ("full", 100), ("full", 1024)])
+def test_plan_eval_levels(kind, size):
+    """The slicing kernel pre-evaluates at most 2 top global levels, only
+    where each part is whole operand words (k1_slice_eval's tiling)."""
+    from paper_2201_10473_b200 import plan
+
+    if os.environ.get("F2X_EVAL_LEVELS"):
+        pytest.skip("override set")
+    p = plan(kind, 4096, size)
+    el = p["eval_levels"]
+    assert 0 <= el <= min(2, p["global_levels"])
+    assert (p["N"] >> el) % 64 == 0
+    if kind == "cyclic":
+        assert el == 2
