@@ -91,8 +91,10 @@ def committed_traffic(pl) -> dict | None:
         except Exception:
             continue
         if d.get("workload") == "n=17669 x4096" and pl.get("leaf_words") == 35:
-            # algorithmic: both bitsliced operands read once + every node product written once
-            ns = pl["leaf_stride"] << pl["levels"]
+            # algorithmic: both (pre-evaluated) bitsliced operands read once + every
+            # node product written once
+            el = pl.get("eval_levels", 0)
+            ns = 3 ** el * (pl["leaf_stride"] << (pl["levels"] - el))
             ss = pl["leaf_stride"] << pl["cta_levels"]
             alg = 4 * pl["groups"] * (2 * ns + 3 ** pl["global_levels"] * 2 * ss)
             best = {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"],
