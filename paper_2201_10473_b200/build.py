@@ -24,6 +24,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xcompiler", "-fvisibility=hidden",
          "-I" + INCLUDE, "-Xptxas", "-warn-spills"]
+# F2X_NVCC_EXTRA: extra nvcc flags for schedule experiments (e.g. -DF2X_FUSED_BOTTOM_EVAL=0);
+# delete _build/ when changing it (objects are cached by mtime)
+FLAGS += os.environ.get("F2X_NVCC_EXTRA", "").split()
 
 
 def sources() -> list[str]:

@@ -156,10 +156,12 @@ template <int EL>
 __global__ void __launch_bounds__(kTileThreads << EL)
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
-              int ncyc, uint32_t *d_err, int tiles) {
+              int ncyc, uint32_t *d_err, int tiles, int TW) {
+    // TW (<= 64) operand words per tile: the part is cut into `tiles`
+    // balanced tiles, so no CTA carries a nearly empty tail tile
     constexpr int NP = 1 << EL;               // parts
     constexpr int NO = EL == 1 ? 3 : 9;       // evaluated sub-operands
-    constexpr int STG = kTileCoeffs + kTileCoeffs / 32;
+    const int STG = 64 * TW + 2 * TW;         // stage words per part (1 pad per 32)
     extern __shared__ uint32_t stage[];       // [NP][STG]
     const int tid = threadIdx.x & (kTileThreads - 1);
     const int j = threadIdx.x / kTileThreads;  // part handled by this thread's 128-group
@@ -170,8 +172,8 @@ k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, ui
     uint32_t *out = (blockIdx.y ? Eb : Ea) + g * (NO * NsE);
     const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
     const int half = tid & 1;
-    const int ul = tile * kTileWords + (tid >> 1);  // word within the part
-    {
+    const int ul = tile * TW + (tid >> 1);  // word within the part
+    if (tid < 2 * TW) {
         const int u = j * (NE / 64) + ul;  // operand word
         uint32_t x[32];
         uint32_t bad = 0;
@@ -194,7 +196,7 @@ k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, ui
         for (int i = 0; i < 32; ++i) stage[j * STG + stg(32 * tid + i)] = x[i];
     }
     __syncthreads();
-    const int k0 = tile * kTileCoeffs, k1 = min(k0 + kTileCoeffs, NE);
+    const int k0 = tile * 64 * TW, k1 = min(k0 + 64 * TW, NE);
     if (k0 >= k1) return;
     int c, r;
     chunk_split(k0, LF, c, r);
@@ -553,27 +555,31 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                                                     pl.leaf_words, pl.leaf_stride, L.Ns, ncyc,
                                                     d_err, tiles);
     } else {
-        const int tiles = int(ceil_div(pl.N >> L.el, kTileCoeffs));
+        // balanced tiles of <= 64 words per part
+        const int pw = (pl.N >> L.el) / 64;
+        const int tiles = int(ceil_div(pw, kTileWords));
+        const int TW = int(ceil_div(pw, tiles));
         dim3 grid(unsigned(G * tiles), 2);
-        const size_t sm = size_t(1 << L.el) * (kTileCoeffs + kTileCoeffs / 32) * 4;
+        const size_t sm = size_t(1 << L.el) * (64 * TW + 2 * TW) * 4;
+        const size_t sm_max = size_t(1 << L.el) * (64 * kTileWords + 2 * kTileWords) * 4;
         static int attr_dev_mask[3] = {0, 0, 0};  // benign race: the attribute set is idempotent
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 31 && !(attr_dev_mask[L.el] & (1 << dev))) {
             const cudaError_t ae = L.el == 1
-                ? cudaFuncSetAttribute(k1_slice_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))
-                : cudaFuncSetAttribute(k1_slice_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+                ? cudaFuncSetAttribute(k1_slice_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max))
+                : cudaFuncSetAttribute(k1_slice_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max));
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             attr_dev_mask[L.el] |= 1 << dev;
         }
         if (L.el == 1) {
             k1_slice_eval<1><<<grid, kTileThreads << 1, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
-                                                                 L.Ns >> 1, ncyc, d_err, tiles);
+                                                                 L.Ns >> 1, ncyc, d_err, tiles, TW);
         } else {
             k1_slice_eval<2><<<grid, kTileThreads << 2, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
-                                                                 L.Ns >> 2, ncyc, d_err, tiles);
+                                                                 L.Ns >> 2, ncyc, d_err, tiles, TW);
         }
     }
     if ((rc = debug_sync(stream, 1))) return rc;
