@@ -617,7 +617,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                 for (int i = 0; i < 6; ++i) a[i] += double(h[b * 8 + i]);
                 nodes += -h[b * 8 + 7];
             }
-            if (nodes < 1) nodes = 1;
+            if (nodes < 1) {  // the kernel was built without the clocks
+                fprintf(f, "F2X_PHASE_PROF: rebuild with F2X_NVCC_EXTRA=-DF2X_PROF_BUILD=1\n");
+                nodes = 1;
+            }
             fprintf(f, "LF=%d KC=%d GL=%d ctas=%d nodes=%lld cycles/node per slot: %.0f %.0f %.0f %.0f %.0f %.0f  (setup load eval leaf interp store)\n",
                     pl.leaf_words, pl.cta_levels, pl.global_levels, rows, nodes, a[0] / nodes,
                     a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes, a[5] / nodes);

@@ -16,6 +16,8 @@ Stages:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -312,10 +314,30 @@ def interp_pair(As, Bs, P, LFS, KC, j):
         Bs[p1: p1 + q] = c1q2
 
 
+def mid_perm(KC: int):
+    """The kernels' mid-leaf assignment (gen_instances.py MID_PERM, KC = 5):
+    chunk Rm + i holds the mid leaf of level-(KC-1) node perm[i]."""
+    if KC != 5:
+        return list(range(pow3(KC - 1))) if KC >= 1 else []
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "gen", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "paper_2201_10473_b200", "csrc", "gen_instances.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    return list(gen.MID_PERM)
+
+
 def k2_v2(plan: Plan, Abs: np.ndarray, Bbs: np.ndarray) -> np.ndarray:
     LF, LFS, KC, GL, Ss = plan.LF, plan.LFS, plan.KC, plan.GL, plan.Ss
     R = LFS * pow3(KC)
     P = leaf_positions(plan)
+    sigma = mid_perm(KC)
+    if KC >= 1:  # mid leaf of node kappa is stored at chunk Rm + sigma^-1(kappa)
+        Rm_w = R - pow3(KC - 1) * LFS
+        for i, kappa in enumerate(sigma):
+            P[KC][3 * kappa + 2] = Rm_w + i * LFS
     out = np.zeros((plan.G, pow3(GL), 2 * Ss), dtype=np.uint32)
     for g in range(plan.G):
         for path in range(pow3(GL)):
@@ -337,7 +359,7 @@ def k2_v2(plan: Plan, Abs: np.ndarray, Bbs: np.ndarray) -> np.ndarray:
             prods = {}
             for ch in range(R // LFS):
                 if KC >= 1 and ch >= Rm:
-                    pp = P[KC - 1][ch - Rm]
+                    pp = P[KC - 1][sigma[ch - Rm]]
                     a = As[pp: pp + LF] ^ As[pp + LFS: pp + LFS + LF]
                     b = Bs[pp: pp + LF] ^ Bs[pp + LFS: pp + LFS + LF]
                 else:

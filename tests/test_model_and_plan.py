@@ -239,3 +239,52 @@ def test_plan_eval_levels(kind, size):
     assert (p["N"] >> el) % 64 == 0
     if kind == "cyclic":
         assert el == 2
+
+
+def _phase_wavefronts(addrs):
+    """Shared-memory wavefronts of 16-byte accesses: a warp's request is
+    served in 8-thread phases, each costing the largest number of threads
+    that hit the same 16-byte bank group (quad index mod 8)."""
+    import collections
+
+    w = 0
+    for b in range(0, len(addrs), 8):
+        c = collections.Counter(a % 8 for a in addrs[b:b + 8] if a is not None)
+        if c:
+            w += max(c.values())
+    return w
+
+
+def test_mid_perm_bank_phases():
+    """gen_instances.MID_PERM is a permutation of the 81 mid leaves (KC=5)
+    that lowers the 8-thread bank phases of the mid leaves' parent reads
+    (1620 -> 1188 weighted wavefronts, 9-quad chunks) and of the level-3/4
+    interpolation's mid-product reads (324 -> 198), as the generator states."""
+    sigma = mb.mid_perm(5)
+    assert sorted(sigma) == list(range(81))
+    inv = [sigma.index(m) for m in range(81)]
+    p = mb.Plan(35, 9, 5, kind="full", t=280, n=0, batch=32)
+    Q, RM = p.LFS // 4, 162
+    P4 = [x // p.LFS for x in mb.leaf_positions(p)[4]]   # chunks
+    P3 = mb.leaf_positions(p)[3]
+
+    def leaf(sig):
+        tot = 0
+        for q in range(Q):
+            for half in (0, 1):
+                addrs = [None if t >= 243 else (t * Q + q if t < RM else (P4[sig[t - RM]] + half) * Q + q)
+                         for t in range(160, 256)]
+                tot += 3 * _phase_wavefronts(addrs)
+        return tot
+
+    def interp(iv):
+        tot = 0
+        for c in range(3):
+            addrs = [None if it >= 27 * Q else (RM + iv[3 * (it // Q) + c]) * Q + it % Q for it in range(256)]
+            tot += 2 * _phase_wavefronts(addrs)
+        return tot
+
+    ident = list(range(81))
+    assert (leaf(ident), interp(ident)) == (1620, 324)
+    assert (leaf(sigma), interp(inv)) == (1188, 198)
+    assert len(P3) == 27
