@@ -257,9 +257,10 @@ def _phase_wavefronts(addrs):
 
 def test_mid_perm_bank_phases():
     """gen_instances.MID_PERM is a permutation of the 81 mid leaves (KC=5)
-    that lowers the 8-thread bank phases of the mid leaves' parent reads
-    (1620 -> 1188 weighted wavefronts, 9-quad chunks) and of the level-3/4
-    interpolation's mid-product reads (324 -> 198), as the generator states."""
+    that, with odd threads reading the parent's hi chunk first, makes the
+    mid leaves' parent reads conflict-free (1620 -> 648 weighted wavefronts,
+    9-quad chunks) and lowers the level-3/4 interpolation's mid-product reads
+    (324 -> 202), as the generator states."""
     sigma = mb.mid_perm(5)
     assert sorted(sigma) == list(range(81))
     inv = [sigma.index(m) for m in range(81)]
@@ -268,11 +269,12 @@ def test_mid_perm_bank_phases():
     P4 = [x // p.LFS for x in mb.leaf_positions(p)[4]]   # chunks
     P3 = mb.leaf_positions(p)[3]
 
-    def leaf(sig):
+    def leaf(sig, stagger):
         tot = 0
         for q in range(Q):
-            for half in (0, 1):
-                addrs = [None if t >= 243 else (t * Q + q if t < RM else (P4[sig[t - RM]] + half) * Q + q)
+            for k in (0, 1):  # first / second load instruction
+                addrs = [None if t >= 243 else
+                         (t * Q + q if t < RM else (P4[sig[t - RM]] + (k ^ (t & 1) if stagger else k)) * Q + q)
                          for t in range(160, 256)]
                 tot += 3 * _phase_wavefronts(addrs)
         return tot
@@ -285,6 +287,6 @@ def test_mid_perm_bank_phases():
         return tot
 
     ident = list(range(81))
-    assert (leaf(ident), interp(ident)) == (1620, 324)
-    assert (leaf(sigma), interp(inv)) == (1188, 198)
+    assert (leaf(ident, False), interp(ident)) == (1620, 324)
+    assert (leaf(sigma, True), interp(inv)) == (648, 202)
     assert len(P3) == 27
