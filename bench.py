@@ -345,12 +345,12 @@ def gpu_arm(args) -> None:
         pipe.run(hAs[i], hBs[i], hCs[i], lane=i)
         e2e_i[0] += 1
 
-    for _ in range(max(2, args.warmup // 2)):
+    for _ in range(max(2 * LANES, args.warmup)):
         e2e_step()
     pipe.join()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    KE = max(3, K // 4)
+    KE = max(3, K // 2)
     e0.record()
     for _ in range(KE):
         e2e_step()
