@@ -125,7 +125,7 @@ def _ref_rows(args):
     return hi - lo, time.perf_counter() - t0
 
 
-def cpu_reference(n: int, rows_per_core: int = 48) -> dict:
+def cpu_reference(n: int, rows_per_core: int = 48, pool=None, c_port: bool = True) -> dict:
     """Reference CPU path on all host cores: the oracle's restatement of
     schoolbook_mul's default (bit-spread big-int) route + SPEC fold, one
     product per row (the reference has no batched API), processes because
@@ -139,8 +139,11 @@ def cpu_reference(n: int, rows_per_core: int = 48) -> dict:
     sample = cores * rows_per_core
     chunks = [(n, i * rows_per_core, (i + 1) * rows_per_core) for i in range(cores)]
     t0 = time.perf_counter()
-    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
-        res = list(ex.map(_ref_rows, chunks))
+    if pool is not None:
+        res = list(pool.map(_ref_rows, chunks))
+    else:
+        with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+            res = list(ex.map(_ref_rows, chunks))
     wall = time.perf_counter() - t0
     done = sum(r[0] for r in res)
     # steady-state rate: rows / max per-worker compute time (excludes pool startup)
@@ -150,6 +153,8 @@ def cpu_reference(n: int, rows_per_core: int = 48) -> dict:
            "sample": f"{done} rows of the n={n} ring workload ({rows_per_core}/core), "
                      f"oracle port of schoolbook_mul default route (spread + CPython int) + SPEC fold",
            "wall_s": round(wall, 2)}
+    if not c_port:
+        return out
     try:
         from oracle import c_mul_cyclic
         from oracle.f2x_oracle import make_cyclic_inputs
@@ -492,13 +497,18 @@ def reference_arm(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    import concurrent.futures as cf
+
     n = args.n
     vals = []
     cb = None
-    for i in range(args.warmup + args.steps):
-        cb = cpu_reference(n, rows_per_core=8 if i < args.warmup else 16)
-        if i >= args.warmup:
-            vals.append(cb["value"])
+    # one worker pool for the whole run (pool start-up is not part of a step)
+    with cf.ProcessPoolExecutor(max_workers=len(os.sched_getaffinity(0))) as pool:
+        for i in range(args.warmup + args.steps):
+            last = i == args.warmup + args.steps - 1
+            cb = cpu_reference(n, rows_per_core=8 if i < args.warmup else 16, pool=pool, c_port=last)
+            if i >= args.warmup:
+                vals.append(cb["value"])
     value = sum(vals) / len(vals)
     cb["value"] = value
     line = {
