@@ -76,6 +76,10 @@ typedef struct f2x_plan {
     int32_t eval_levels;     /* top global levels pre-evaluated by the slicing
                                 kernel (node kernel runs on 3^eval_levels x
                                 the groups with levels - eval_levels)        */
+    int32_t toom_levels;     /* Toom-3 levels above the Karatsuba node problem
+                                (node kernel runs on 5^toom_levels x groups) */
+    int32_t toom_w;          /* Toom-3 point x = X^toom_w                      */
+    int32_t toom_M[4];       /* part size (coefficients) of Toom level 1..     */
 } f2x_plan;
 
 /* Fill *plan for a call shape.  leaf_hint = 0 picks the default leaf;

@@ -59,11 +59,15 @@ class F2xPlan(ctypes.Structure):
         ("leaf_ops_per_product", ctypes.c_double),
         ("karatsuba_ops_per_product", ctypes.c_double),
         ("eval_levels", ctypes.c_int32),
+        ("toom_levels", ctypes.c_int32),
+        ("toom_w", ctypes.c_int32),
+        ("toom_M", ctypes.c_int32 * 4),
     ]
 
     def as_dict(self) -> dict:
         d = {name: getattr(self, name) for name, _ in self._fields_}
         d["pass_levels"] = list(self.pass_levels)[: self.num_passes]
+        d["toom_M"] = list(self.toom_M)[: self.toom_levels]
         return d
 
 

@@ -41,9 +41,17 @@ static constexpr int kMaxKC = 5;
 static constexpr int kMaxGL = 8;
 static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
+static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
+static constexpr int kToomW = 16;       // x = X^w (coefficients)
+static constexpr double kToomWordCost = 30.0;  // planner: cost units per word moved (fit on B200)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+static inline int64_t ipow5(int k) {
+    int64_t r = 1;
+    while (k-- > 0) r *= 5;
+    return r;
+}
 static inline int64_t ipow3(int k) {
     int64_t r = 1;
     while (k-- > 0) r *= 3;
@@ -227,6 +235,231 @@ k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, ui
     }
 }
 
+// --------------------------------------------------------------- Toom-3
+// One Toom-3 evaluation level (paper Appendix D): operand
+// item i (3M coefficients, plain bitsliced, stride inS) -> items 5i+e,
+// e = 0, 1, x, x+1, inf with x = X^w, of S >= M + 2w coefficients in the
+// (LFo, LFSo) chunked layout (plain when LFo == LFSo), stride outS.  In the
+// bitsliced layout multiplying by x is an index shift, so each output word is
+// an XOR of at most 5 input words.  Both operands (blockIdx.y).
+__global__ void __launch_bounds__(256)
+toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
+                uint32_t *__restrict__ Yb, int64_t items_in, int64_t inS, int M, int w, int S, int LFo,
+                int LFSo, int64_t outS) {
+    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= items_in * outS) return;
+    const int64_t i = idx / outS;
+    const int sw = int(idx - i * outS);
+    int k;
+    bool valid;
+    if (LFo == LFSo) {
+        k = sw;
+        valid = k < S;
+    } else {
+        const int c = sw / LFSo, r = sw - c * LFSo;
+        k = c * LFo + r;
+        valid = r < LFo && k < S;
+    }
+    const uint32_t *x = (blockIdx.y ? Xb : Xa) + i * inS;
+    uint32_t a0 = 0, a1 = 0, a2 = 0, s1 = 0, s2 = 0;
+    if (valid) {
+        if (k < M) {
+            a0 = __ldg(x + k);
+            a1 = __ldg(x + M + k);
+            a2 = __ldg(x + 2 * M + k);
+        }
+        if (k >= w && k - w < M) s1 = __ldg(x + M + k - w);
+        if (k >= 2 * w && k - 2 * w < M) s2 = __ldg(x + 2 * M + k - 2 * w);
+    }
+    uint32_t *y = (blockIdx.y ? Yb : Ya) + i * 5 * outS + sw;
+    const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
+    y[0] = a0;
+    y[outS] = p1;
+    y[2 * outS] = a0 ^ xs;
+    y[3 * outS] = p1 ^ xs;
+    y[4 * outS] = a2;
+}
+
+// One Toom-3 interpolation level, from the 5 products C_e of every output
+// item i (items 5i+e, Lin coefficients in the (LFi, LFSi) layout, stride inS)
+// to R = c0 + c1 y + c2 y^2 + c3 y^3 + c4 y^4, y = X^M (6M coefficients,
+// plain, stride outS).  Grouped numerators: after
+// the exact division by x, each numerator u_j is a 4-term XOR of inputs and
+// the exact division by x + 1 = 1 + X^w is a prefix XOR along the w chains
+// k = r (mod w):
+//   c3 = scan(u3),                            u3[k] = (C0+C1+Cx+Cx1)[k+w]
+//   c2 = scan(u2) + (1 + x + x^2) Cinf,       u2[k] = C1[k+w] + Cx[k] + Cx1[k+w] + Cx1[k]
+//   c1 = C0 + C1 + scan(u1) + (x + x^2) Cinf, u1[k] = C0[k+w] + Cx[k+w] + Cx[k] + Cx1[k]
+// Two kernels: (A) per block of kToomBlk coefficients, u1..u3 and their
+// block-local chain scans (written to Q) plus each chain's block total;
+// (B) per block of outputs, the carries (XOR of earlier blocks' totals) and
+// the assembly of R from two c_j terms per coefficient.
+constexpr int kToomBlk = 2048;   // coefficients per block (multiple of w)
+constexpr int kToomSeg = 4;      // scan segments per chain and block (3 w kToomSeg <= threads)
+constexpr int kToomScanT = 256;  // threads of the scan kernel
+
+struct ToomIn {
+    const uint32_t *C;  // item base (5 products)
+    int64_t inS;
+    int LFi, LFSi, Lin;
+    float invLF;
+    __device__ __forceinline__ uint32_t rd(int e, int k) const {
+        if (k < 0 || k >= Lin) return 0u;
+        if (LFi == LFSi) return __ldg(C + e * inS + k);
+        // exact: k < 2^24, LF <= 64 (fraction >= 0.5/LF from an integer)
+        const int c = __float2int_rz((float(k) + 0.5f) * invLF);
+        return __ldg(C + e * inS + int64_t(c) * LFSi + (k - c * LFi));
+    }
+};
+
+// Kernel A: block b of item i.  The block's inputs (5 products over
+// [k0 - 2w, k0 + B + w)) are staged in shared memory once; u1..u3 are scanned
+// along their chains inside the block; Q receives c0, c1..c3 without the
+// carry from earlier blocks, and c4 (5 x 2M words per item); Tot receives
+// each chain's block total.
+__global__ void __launch_bounds__(kToomScanT)
+toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uint32_t *__restrict__ Tot, int M,
+                 int w, int LFi, int LFSi, int64_t inS, int Lin, int nb) {
+    extern __shared__ uint32_t tsm[];
+    const int H = kToomBlk + 3 * w;          // staged span per input
+    uint32_t *Stg = tsm;                      // [5][H], index k - (k0 - 2w)
+    uint32_t *U = tsm + 5 * H;                // [3][kToomBlk]
+    __shared__ uint32_t segtot[3][32][kToomSeg];
+    const int64_t item = blockIdx.x / nb;
+    const int b = int(blockIdx.x - item * nb);
+    const int L = 2 * M, k0 = b * kToomBlk, kb = k0 - 2 * w;
+    const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
+    // staging: all of a thread's loads (5 inputs x ceil(H/256)) are issued
+    // before the first shared-memory store -- one memory round trip per CTA
+    {
+        constexpr int T = kToomScanT, NI = (kToomBlk + 3 * kToomW + T - 1) / T;
+        const bool plain = LFi == LFSi;
+        uint32_t v[5][NI];
+#pragma unroll
+        for (int e = 0; e < 5; ++e) {
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int h = int(threadIdx.x) + i * T, k = kb + h;
+                uint32_t x = 0;
+                if (h < H && k >= 0 && k < Lin) {
+                    int64_t off = k;
+                    if (!plain) {
+                        const int c = __float2int_rz((float(k) + 0.5f) * in.invLF);
+                        off = int64_t(c) * LFSi + (k - c * LFi);
+                    }
+                    x = __ldg(in.C + e * inS + off);
+                }
+                v[e][i] = x;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 5; ++e) {
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int h = int(threadIdx.x) + i * T;
+                if (h < H) Stg[e * H + h] = v[e][i];
+            }
+        }
+    }
+    __syncthreads();
+    auto S = [&](int e, int k) -> uint32_t { return Stg[e * H + (k - kb)]; };
+    for (int i = threadIdx.x; i < kToomBlk; i += blockDim.x) {
+        const int k = k0 + i;
+        const uint32_t c0w = S(0, k + w), c1w = S(1, k + w), cxw = S(2, k + w), cx1w = S(3, k + w),
+                       cx = S(2, k), cx1 = S(3, k);
+        U[i] = c0w ^ cxw ^ cx ^ cx1;                    // u1
+        U[kToomBlk + i] = c1w ^ cx ^ cx1w ^ cx1;        // u2
+        U[2 * kToomBlk + i] = c0w ^ c1w ^ cxw ^ cx1w;   // u3
+    }
+    __syncthreads();
+    // chains: 3 numerators x w residues, each cut into kToomSeg segments
+    const int per = kToomBlk / w, segl = per / kToomSeg, nthr = 3 * w * kToomSeg;
+    const int t = threadIdx.x;
+    int j = 0, r = 0, sg = 0;
+    if (t < nthr) {
+        j = t / (w * kToomSeg);
+        r = (t / kToomSeg) % w;
+        sg = t % kToomSeg;
+        uint32_t acc = 0;
+        for (int e = sg * segl; e < (sg + 1) * segl; ++e) {
+            const int i = j * kToomBlk + r + e * w;
+            acc ^= U[i];
+            U[i] = acc;
+        }
+        segtot[j][r][sg] = acc;
+    }
+    __syncthreads();
+    if (t < nthr) {
+        uint32_t carry = 0;
+        for (int s2 = 0; s2 < sg; ++s2) carry ^= segtot[j][r][s2];
+        for (int e = sg * segl; e < (sg + 1) * segl; ++e) U[j * kToomBlk + r + e * w] ^= carry;
+    }
+    __syncthreads();
+    uint32_t *q = Q + item * 5 * int64_t(L);
+    for (int i = threadIdx.x; i < kToomBlk; i += blockDim.x) {
+        const int k = k0 + i;
+        if (k < L) {
+            const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = S(4, k - w) ^ S(4, k - 2 * w);
+            q[k] = c0;
+            q[L + k] = U[i] ^ c0 ^ S(1, k) ^ c4w;          // c1 (no carry)
+            q[2 * L + k] = U[kToomBlk + i] ^ c4 ^ c4w;    // c2 (no carry)
+            q[3 * L + k] = U[2 * kToomBlk + i];           // c3 (no carry)
+            q[4 * L + k] = c4;
+        }
+    }
+    if (threadIdx.x < 3 * w) {  // block totals: last element of each chain
+        const int jj = threadIdx.x / w, rr = threadIdx.x % w;
+        Tot[(item * nb + b) * 3 * w + threadIdx.x] = U[jj * kToomBlk + kToomBlk - w + rr];
+    }
+}
+
+// Kernel B: output block ob of item i.  R[k] = c_a[k - aM] + c_{a-1}[k - (a-1)M]
+// (a = k / M), the c_1..c_3 terms plus their chain carries (XOR of the earlier
+// blocks' totals).
+__global__ void __launch_bounds__(256)
+toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict__ Tot, uint32_t *__restrict__ R,
+                     int M, int w, int nb, int nbo, int64_t outS) {
+    extern __shared__ uint32_t carry[];  // [nb][3][w]
+    const int64_t item = blockIdx.x / nbo;
+    const int ob = int(blockIdx.x - item * nbo);
+    const int L = 2 * M;
+    const uint32_t *tot = Tot + item * nb * 3 * w;
+    for (int c = threadIdx.x; c < 3 * w; c += blockDim.x) {
+        uint32_t acc = 0;
+        for (int b = 0; b < nb; ++b) {
+            carry[b * 3 * w + c] = acc;
+            acc ^= __ldg(tot + b * 3 * w + c);
+        }
+    }
+    __syncthreads();
+    const uint32_t *q = Q + item * 5 * int64_t(L);
+    auto cj = [&](int j, int k) -> uint32_t {
+        uint32_t v = __ldg(q + j * int64_t(L) + k);
+        if (j >= 1 && j <= 3) v ^= carry[(k / kToomBlk) * 3 * w + (j - 1) * w + (k & (w - 1))];
+        return v;
+    };
+    uint32_t *out = R + item * outS;
+    const int kend = min((ob + 1) * kToomBlk, 6 * M);
+    constexpr int NI = kToomBlk / 256;  // outputs per thread, all loads in flight
+    uint32_t v[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int kk = ob * kToomBlk + int(threadIdx.x) + i * 256;
+        const int a = (kk >= M) + (kk >= 2 * M) + (kk >= 3 * M) + (kk >= 4 * M) + (kk >= 5 * M);
+        uint32_t x = 0;
+        if (kk < kend) {
+            if (a <= 4) x ^= cj(a, kk - a * M);
+            if (a >= 1) x ^= cj(a - 1, kk - (a - 1) * M);
+        }
+        v[i] = x;
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int kk = ob * kToomBlk + int(threadIdx.x) + i * 256;
+        if (kk < kend) out[kk] = v[i];
+    }
+}
+
 // ------------------------------------------------------------------- K3
 // Global Karatsuba interpolation, D levels in one pass.  Node products are
 // split into 4 quarters; a node's quarter index w only touches its
@@ -337,10 +570,18 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
 }
 
 // ---------------------------------------------------------------- planner
+
 struct Layout {
     int64_t Ns, Ss;
     int64_t off_abs, off_bbs, off_p0, off_p1, total;
-    int el;  // pre-evaluated top global levels (K1b)
+    int el;                          // pre-evaluated top global levels (K1b)
+    int tl = 0;                      // Toom-3 levels
+    int64_t G2 = 0;                  // node-problem groups (G 5^tl)
+    int64_t M[kMaxToom + 1] = {};    // Toom part sizes, level 1..tl
+    int64_t off_x[kMaxToom] = {};    // Toom operands: [0] plain slice, [l] level-l outputs
+    int64_t off_r[kMaxToom + 1] = {};  // Toom interpolation outputs, level l
+    int64_t off_q[kMaxToom + 1] = {};  // level-l c_0..c_4 before carries (5 x 2M per item)
+    int64_t off_tot[kMaxToom + 1] = {};  // level-l chain totals per block
 };
 
 // Top global levels pre-evaluated by the slicing kernel (k1_slice_eval):
@@ -359,6 +600,58 @@ static int eval_levels_for(int GL, int64_t N) {
     return el;
 }
 
+// Leaf size LF and Karatsuba depth K for a node problem of >= Smin
+// coefficients: minimises 3^K (LF^2 + 48 LF) (leaf LOP3 + the per-leaf
+// tree overhead, ~48 LOP3-equivalents per leaf word measured on B200).
+static bool best_leaf(int64_t Smin, int leaf_hint, int &bestLF, int &bestK, double &best) {
+    bestLF = 0;
+    const int maxK = kMaxKC + kMaxGL;
+    for (int K = 1; K <= maxK; ++K) {
+        int64_t LF = ceil_div(Smin, int64_t(1) << K);
+        if (K >= kMaxKC) {
+            if (LF < 16) LF = 16;
+            if (LF > 40) continue;
+        } else {
+            LF = LF <= 16 ? 16 : (LF <= 32 ? 32 : 0);
+            if (!LF) continue;
+        }
+        if (leaf_hint) {
+            if (LF > leaf_hint) continue;
+            LF = leaf_hint;
+        }
+        const int KC = std::min(K, kMaxKC);
+        if (!find_k2(int(LF), KC)) continue;
+        const double cost = double(ipow3(K)) * double(LF * LF + 48 * LF);
+        if (!bestLF || cost < best) {
+            best = cost;
+            bestLF = int(LF);
+            bestK = K;
+        }
+        if (leaf_hint) break;  // smallest K that fits the forced leaf
+    }
+    return bestLF != 0;
+}
+
+// Toom-3 top levels (TL): level l splits an operand of 3 M_l coefficients
+// into thirds and evaluates at 0, 1, x, x+1, inf (x = X^w): 5 operands of
+// S_l >= M_l + 2w coefficients; S_l = 3 M_{l+1} below another Toom level,
+// the node size LF 2^K at the last.  Sizes for Nmin coefficients:
+static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
+    M[1] = ceil_div(Nmin, 3);
+    for (int l = 1; l < TL; ++l) M[l + 1] = ceil_div(M[l] + 2 * kToomW, 3);
+    Smin_last = M[TL] + 2 * kToomW;
+}
+
+// F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
+static int toom_override() {
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("F2X_TOOM");
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : -1;
+    }
+    return v;
+}
+
 static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
                      Layout *lay) {
     if (!pl || batch < 1 || t_or_n < 1) return F2X_EINVAL;
@@ -375,44 +668,48 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         return F2X_EINVAL;
     }
     const int64_t Nmin = int64_t(64) * t;
-    int bestLF = 0, bestK = 0;
+    // candidates: 0..kMaxToom Toom-3 levels on top of the Karatsuba node problem
+    int bestTL = -1, bestLF = 0, bestK = 0;
     double best = 0;
-    for (int K = 1; K <= kMaxKC + kMaxGL; ++K) {
-        int64_t LF = ceil_div(Nmin, int64_t(1) << K);
-        if (K >= kMaxKC) {
-            if (LF < 16) LF = 16;
-            if (LF > 40) continue;
-        } else {
-            LF = LF <= 16 ? 16 : (LF <= 32 ? 32 : 0);
-            if (!LF) continue;
+    int64_t bestM[kMaxToom + 1] = {0};
+    const int forced = leaf_hint ? 0 : toom_override();
+    for (int TL = 0; TL <= kMaxToom; ++TL) {
+        if (forced >= 0 && TL != forced) continue;
+        if (TL > 0 && leaf_hint) continue;
+        int64_t M[kMaxToom + 1] = {0}, Smin = Nmin;
+        if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
+        int LF, K;
+        double c;
+        if (!best_leaf(Smin, leaf_hint, LF, K, c)) continue;
+        c *= double(ipow5(TL));
+        // Toom passes are HBM-bound: ~kToomWordCost per word moved per group
+        for (int l = 1; l <= TL; ++l) {
+            const double Sl = l < TL ? 3.0 * double(M[l + 1]) : double(int64_t(LF) << K);
+            const double ev = 2.0 * double(ipow5(l - 1)) * 3.0 * double(M[l]) + 2.0 * double(ipow5(l)) * Sl;
+            const double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
+            c += kToomWordCost * (ev + ip);
         }
-        if (leaf_hint) {
-            if (LF > leaf_hint) continue;
-            LF = leaf_hint;
-        }
-        const int KC = std::min(K, kMaxKC);
-        if (!find_k2(int(LF), KC)) continue;
-        // leaf LOP3 (LF^2 per leaf) + per-leaf Karatsuba/tree overhead, which
-        // measured on B200 is worth ~48 LOP3 per leaf word (tools/quick_time)
-        const double cost = double(ipow3(K)) * double(LF * LF + 48 * LF);
-        if (!bestLF || cost < best) {
-            best = cost;
-            bestLF = int(LF);
+        if (bestTL < 0 || c < best) {
+            best = c;
+            bestTL = TL;
+            bestLF = LF;
             bestK = K;
+            std::memcpy(bestM, M, sizeof(M));
         }
-        if (leaf_hint) break;  // smallest K that fits the forced leaf
     }
-    if (!bestLF) return F2X_ERANGE;
-    const int LF = bestLF, K = bestK, KC = std::min(K, kMaxKC), GL = K - KC;
+    if (bestTL < 0) return F2X_ERANGE;
+    const int TL = bestTL, LF = bestLF, K = bestK, KC = std::min(K, kMaxKC), GL = K - KC;
     const K2Entry *e = find_k2(LF, KC);
     const int LFS = leaf_stride_words(LF);
+    const int64_t G = ceil_div(batch, 32);
+    const int64_t G2 = G * ipow5(TL);  // node-problem groups
 
     pl->kind = kind;
     pl->t = t;
     pl->n = n;
-    pl->N = LF << K;
+    pl->N = TL ? int32_t(3 * bestM[1]) : (LF << K);
     pl->batch = batch;
-    pl->groups = ceil_div(batch, 32);
+    pl->groups = G;
     pl->leaf_words = LF;
     pl->leaf_stride = LFS;
     pl->levels = K;
@@ -425,12 +722,15 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         rem -= p;
     }
     pl->num_passes = np;
-    pl->launches = 3 + np;
+    pl->launches = 3 + np + 2 * TL;
     pl->cta_threads = e->threads;
-    pl->node_ctas = pl->groups * ipow3(GL);
+    pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
+    pl->toom_levels = TL;
+    pl->toom_w = TL ? kToomW : 0;
+    for (int l = 1; l <= TL; ++l) pl->toom_M[l - 1] = int32_t(bestM[l]);
     // analytic operation counts per product (bitsliced: 1 LOP3 = 32 products)
-    pl->leaf_ops_per_product = double(ipow3(K)) * LF * LF / 32.0;
+    pl->leaf_ops_per_product = double(ipow5(TL)) * double(ipow3(K)) * LF * LF / 32.0;
     {
         // eval: each level-j node writes one mid of h_j words per operand;
         // interp: 3 XOR-ops per half word.  Summed over all K levels.
@@ -440,30 +740,51 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
             ev += 2.0 * double(ipow3(j)) * hj;
             ip += 3.0 * double(ipow3(j)) * hj;
         }
-        pl->karatsuba_ops_per_product = (ev + ip) / 32.0;
+        pl->karatsuba_ops_per_product = double(ipow5(TL)) * (ev + ip) / 32.0;
     }
     Layout L;
+    L.tl = TL;
+    L.G2 = G2;
+    for (int l = 0; l <= kMaxToom; ++l) L.M[l] = bestM[l];
     L.Ns = int64_t(LFS) << K;
     L.Ss = int64_t(LFS) << KC;
-    const int64_t G = pl->groups;
-    L.el = eval_levels_for(GL, int64_t(LF) << K);
-    const int64_t opw = G * ipow3(L.el) * (L.Ns >> L.el);  // operand words (evaluated)
-    L.off_abs = 0;
+    L.el = TL ? 0 : eval_levels_for(GL, int64_t(LF) << K);
+    int64_t off = 0;
+    if (TL > 0) {  // plain bitsliced operand and the upper Toom levels' operands
+        L.off_x[0] = off;
+        off = align256(off + 2 * G * 3 * L.M[1] * 4);
+        for (int l = 1; l < TL; ++l) {
+            L.off_x[l] = off;
+            off = align256(off + 2 * G * ipow5(l) * 3 * L.M[l + 1] * 4);
+        }
+    }
+    const int64_t opw = G2 * ipow3(L.el) * (L.Ns >> L.el);  // node-problem operand words
+    L.off_abs = off;
     L.off_bbs = align256(L.off_abs + opw * 4);
     L.off_p0 = align256(L.off_bbs + opw * 4);
-    const int64_t p0 = G * ipow3(GL) * 2 * L.Ss * 4;
+    const int64_t p0 = G2 * ipow3(GL) * 2 * L.Ss * 4;
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
     if (np >= 1) {  // first pass output (the largest one written to P1)
         const int d1 = GL - pl->pass_levels[0];
-        p1 = G * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
+        p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
-    L.total = align256(L.off_p1 + p1);
+    off = align256(L.off_p1 + p1);
+    for (int l = TL; l >= 1; --l) {  // Toom interpolation: block scans, totals, outputs
+        const int64_t items = G * ipow5(l - 1);
+        L.off_q[l] = off;
+        off = align256(off + items * 5 * 2 * L.M[l] * 4);
+        L.off_tot[l] = off;
+        off = align256(off + items * ceil_div(2 * L.M[l], kToomBlk) * 3 * kToomW * 4);
+        L.off_r[l] = off;
+        off = align256(off + items * 6 * L.M[l] * 4);
+    }
+    L.total = off;
     {  // every pass output must fit the ping-pong buffer it is written to
         int d = GL;
         for (int i = 0; i < np; ++i) {
             const int dlo = d - pl->pass_levels[i];
-            const int64_t outb = G * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
+            const int64_t outb = G2 * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
             if (outb > ((i & 1) ? p0 : p1)) return F2X_ERANGE;
             d = dlo;
         }
@@ -547,8 +868,45 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     const int64_t G = pl.groups;
     const int ncyc = kind == F2X_KIND_CYCLIC ? pl.n : 0;
 
-    // K1 (with the top L.el global levels pre-evaluated when L.el > 0)
-    if (L.el == 0) {
+    // K1 (with the top L.el global levels pre-evaluated when L.el > 0;
+    // Toom plans slice to a plain operand of N = 3 M_1 coefficients)
+    if (L.tl > 0) {
+        const int tiles = int(ceil_div(pl.N, kTileCoeffs));
+        dim3 grid(unsigned(G * tiles), 2);
+        uint32_t *X0a = reinterpret_cast<uint32_t *>(w + L.off_x[0]);
+        k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, X0a, X0a + G * int64_t(pl.N), batch, pl.t, pl.N,
+                                                    pl.N, pl.N, int64_t(pl.N), ncyc, d_err, tiles);
+        if ((rc = debug_sync(stream, 1))) return rc;
+        // Toom evaluation levels: level l < tl writes plain operands of
+        // 3 M_{l+1} coefficients, the last one the node problem's chunked
+        // operands (LF 2^K coefficients)
+        for (int l = 1; l <= L.tl; ++l) {
+            const uint32_t *xa = reinterpret_cast<const uint32_t *>(w + L.off_x[l - 1]);
+            const int64_t items_in = G * ipow5(l - 1), inS = 3 * L.M[l];
+            const uint32_t *xb = xa + items_in * inS;
+            uint32_t *ya, *yb;
+            int S, LFo, LFSo;
+            int64_t outS;
+            if (l < L.tl) {
+                ya = reinterpret_cast<uint32_t *>(w + L.off_x[l]);
+                S = int(3 * L.M[l + 1]);
+                LFo = LFSo = S;
+                outS = S;
+                yb = ya + items_in * 5 * outS;
+            } else {
+                ya = Abs;
+                yb = Bbs;
+                S = pl.leaf_words << pl.levels;
+                LFo = pl.leaf_words;
+                LFSo = pl.leaf_stride;
+                outS = L.Ns;
+            }
+            dim3 grid(unsigned(ceil_div(items_in * outS, 256)), 2);
+            toom_eval_level<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
+                                                      S, LFo, LFSo, outS);
+            if ((rc = debug_sync(stream, 1))) return rc;
+        }
+    } else if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
         k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
@@ -635,7 +993,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int dlo = d - D;
         const int64_t Shi = L.Ns >> d, Slo = L.Ns >> dlo;
         const int qw = int(Shi / 2);
-        const int64_t items = G * ipow3(dlo) * qw;
+        const int64_t items = L.G2 * ipow3(dlo) * qw;
         switch (D) {
             case 1: launch_k3<1>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
             case 2: launch_k3<2>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
@@ -654,12 +1012,46 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         std::swap(cur, nxt);
         d = dlo;
     }
+    // Toom interpolation levels, innermost first: level tl reads the node
+    // problem's chunked root products, the others the plain 6 M_{l+1}
+    // products of the level below
+    const uint32_t *root = cur;
+    int rootLF = pl.leaf_words, rootLFS = pl.leaf_stride;
+    int64_t rootS = 2 * L.Ns;
+    for (int l = L.tl; l >= 1; --l) {
+        uint32_t *out = reinterpret_cast<uint32_t *>(w + L.off_r[l]);
+        uint32_t *Q = reinterpret_cast<uint32_t *>(w + L.off_q[l]);
+        uint32_t *Tot = reinterpret_cast<uint32_t *>(w + L.off_tot[l]);
+        const int M = int(L.M[l]);
+        const int64_t items = G * ipow5(l - 1), outS = 6 * int64_t(M);
+        const int Lin = l == L.tl ? (2 * pl.leaf_words) << pl.levels : int(6 * L.M[l + 1]);
+        const int nb = int(ceil_div(2 * M, kToomBlk)), nbo = int(ceil_div(6 * M, kToomBlk));
+        const size_t sms = (size_t(5) * (kToomBlk + 3 * kToomW) + size_t(3) * kToomBlk) * 4;
+        static int attr_dev_mask = 0;  // benign race: the attribute set is idempotent
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 31 && !(attr_dev_mask & (1 << dev))) {
+            const cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        int(sms));
+            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
+            attr_dev_mask |= 1 << dev;
+        }
+        toom_interp_scan<<<unsigned(items * nb), kToomScanT, sms, stream>>>(root, Q, Tot, M, kToomW, rootLF, rootLFS,
+                                                                     rootS, Lin, nb);
+        if ((rc = debug_sync(stream, 5))) return rc;
+        const size_t sm = size_t(nb) * 3 * kToomW * 4;
+        toom_interp_assemble<<<unsigned(items * nbo), 256, sm, stream>>>(Q, Tot, out, M, kToomW, nb, nbo, outS);
+        if ((rc = debug_sync(stream, 5))) return rc;
+        root = out;
+        rootLF = rootLFS = int(outS);
+        rootS = outS;
+    }
     // K4
     {
         const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
         const int tiles = int(ceil_div(tout, kTileWords));
         k4_unslice<<<unsigned(G * tiles), kTileThreads, 0, stream>>>(
-            cur, C, batch, tout, pl.leaf_words, pl.leaf_stride, 2 * L.Ns, ncyc, tiles);
+            root, C, batch, tout, rootLF, rootLFS, rootS, ncyc, tiles);
     }
     if ((rc = debug_sync(stream, 4))) return rc;
     const cudaError_t ce = cudaGetLastError();

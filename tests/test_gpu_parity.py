@@ -331,7 +331,45 @@ def test_eval_levels_override(el, cuda):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, F2X_EVAL_LEVELS=str(el))
+    env = dict(os.environ, F2X_EVAL_LEVELS=str(el), F2X_TOOM="0")  # Karatsuba-only plans
     r = subprocess.run([sys.executable, "-c", _EL_SCRIPT, root, str(el)], env=env,
                        capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+_TOOM_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import c_mul_cyclic, c_mul_full
+from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+tl = int(sys.argv[2])
+dev = torch.device("cuda", 0)
+d = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)
+for n, b in ((1000, 7), (12323, 70), (17669, 64), (35851, 33), (57637, 40)):
+    assert plan("cyclic", b, n)["toom_levels"] == tl
+    A, B = make_cyclic_inputs(n, b)
+    out = mul_cyclic(d(A), d(B), n).cpu().numpy().view(np.uint64)
+    assert np.array_equal(out, c_mul_cyclic(A, B, n)), n
+for t, b in ((16, 33), (64, 40), (277, 5), (1024, 40)):
+    A, B = make_full_inputs(t, b, words=True)
+    out = mul_full(d(A), d(B)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(out, c_mul_full(A, B)), t
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("tl", [0, 1, 2, 3])
+def test_toom_levels_forced(tl, cuda):
+    """Toom-3 levels above the Karatsuba node problem (F2X_TOOM, read once per
+    process): 0-3 levels give the oracle's bits for ring and full sizes,
+    ragged batches included."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, F2X_TOOM=str(tl))
+    r = subprocess.run([sys.executable, "-c", _TOOM_SCRIPT, root, str(tl)], env=env,
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

@@ -195,14 +195,15 @@ def test_plan_counts_match_closed_forms(lib, kind, size):
     """Counter conservation (Table 1): the plan's analytic counts
     follow the KaratRec closed forms -- 3^K leaf products of LF x LF
     coefficients (LF^2/32 LOP3 each per product, bitsliced over 32), and
-    eval+interp XOR work sum_j 3^j * 5 * LF*2^(K-j-1) / 32 per product."""
+    eval+interp XOR work sum_j 3^j * 5 * LF*2^(K-j-1) / 32 per product; with
+    Toom-3 levels on top, 5^toom_levels node problems per product."""
     from paper_2201_10473_b200 import _lib
 
     pl = _lib.make_plan(kind, 4096, size)
-    LF, K = pl.leaf_words, pl.levels
-    assert pl.leaf_ops_per_product == pytest.approx(3 ** K * LF * LF / 32)
+    LF, K, T = pl.leaf_words, pl.levels, 5 ** pl.toom_levels
+    assert pl.leaf_ops_per_product == pytest.approx(T * 3 ** K * LF * LF / 32)
     xors = sum(3 ** j * 5 * (LF << (K - j - 1)) for j in range(K)) / 32
-    assert pl.karatsuba_ops_per_product == pytest.approx(xors)
+    assert pl.karatsuba_ops_per_product == pytest.approx(T * xors)
     # KaratRec base-multiplication count for 2^K leaves is 3^K (Table 1, t^log2(3))
     assert round((2 ** K) ** np.log2(3)) == 3 ** K
 
@@ -236,6 +237,9 @@ def test_plan_eval_levels(kind, size):
     p = plan(kind, 4096, size)
     el = p["eval_levels"]
     assert 0 <= el <= min(2, p["global_levels"])
+    if p["toom_levels"]:  # Toom plans slice plainly; the node kernel walks its levels
+        assert el == 0
+        return
     assert (p["N"] >> el) % 64 == 0
     if kind == "cyclic":
         assert el == 2
@@ -290,3 +294,52 @@ def test_mid_perm_bank_phases():
     assert (leaf(ident, False), interp(ident)) == (1620, 324)
     assert (leaf(sigma, True), interp(inv)) == (648, 202)
     assert len(P3) == 27
+
+
+@pytest.mark.parametrize("levels_spec", [[(20, 3)], [(37, 8)], [(64, 16)], [(50, 1)],
+                                         [(60, 4), None], [(40, 2), None, None]])
+def test_toom_model_matches_oracle(levels_spec):
+    """tests/model_toom.py: bitsliced Toom-3 (points 0, 1, x, x+1, inf with
+    x = X^w, SURVEY Appx A.2 grouped numerators, exact divisions asserted)
+    over 1-3 levels equals the oracle product for 32 random products."""
+    import model_toom as mt
+
+    M1, w = levels_spec[0]
+    levels = []
+    M = M1
+    for i in range(len(levels_spec)):
+        S = M + 2 * w
+        if i + 1 < len(levels_spec):
+            S = 3 * (-(-S // 3))
+        levels.append((M, w, S))
+        M = S // 3
+    rng = np.random.default_rng(M1 * 7 + w)
+    t = (3 * M1) // 64 + 1
+    A = rng.integers(0, 1 << 64, (32, t), dtype=np.uint64)
+    B = rng.integers(0, 1 << 64, (32, t), dtype=np.uint64)
+    a, b = mt.slice32(A, 3 * M1), mt.slice32(B, 3 * M1)
+    ref = o.mul_full(mt.unslice32(a, 32, t), mt.unslice32(b, 32, t))
+    assert np.array_equal(mt.unslice32(mt.toom_mul(a, b, levels), 32, 2 * t), ref)
+
+
+@pytest.mark.parametrize("kind,size", [("cyclic", 17669), ("cyclic", 57637), ("full", 1024)])
+@pytest.mark.parametrize("tl", [1, 2, 3])
+def test_toom_plan_sizes(kind, size, tl):
+    """Forced Toom plans (F2X_TOOM is read once per process, so the sizes are
+    recomputed here from the same rule): 3 M_1 >= 64 t, S_l = 3 M_{l+1} >=
+    M_l + 2w, and the node problem LF 2^K >= M_tl + 2w."""
+    t = (size + 63) // 64 if kind == "cyclic" else size
+    w = 16
+    M = [0, -(-64 * t // 3)]
+    for _ in range(1, tl):
+        M.append(-(-(M[-1] + 2 * w) // 3))
+    assert 3 * M[1] >= 64 * t
+    for l in range(1, tl):
+        assert 3 * M[l + 1] >= M[l] + 2 * w
+    from paper_2201_10473_b200 import plan
+
+    p = plan(kind, 4096, size)
+    if p["toom_levels"]:
+        Ms = p["toom_M"]
+        assert 3 * Ms[0] >= 64 * t and len(Ms) == p["toom_levels"]
+        assert p["leaf_words"] << p["levels"] >= Ms[-1] + 2 * p["toom_w"]
