@@ -323,8 +323,6 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     extern __shared__ uint32_t tsm[];
     const int H = kToomBlk + 3 * w;          // staged span per input
     uint32_t *Stg = tsm;                      // [5][H], index k - (k0 - 2w)
-    uint32_t *U = tsm + 5 * H;                // [3][kToomBlk]
-    __shared__ uint32_t segtot[3][32][kToomSeg];
     const int64_t item = blockIdx.x / nb;
     const int b = int(blockIdx.x - item * nb);
     const int L = 2 * M, k0 = b * kToomBlk, kb = k0 - 2 * w;
@@ -363,53 +361,64 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     }
     __syncthreads();
     auto S = [&](int e, int k) -> uint32_t { return Stg[e * H + (k - kb)]; };
-    for (int i = threadIdx.x; i < kToomBlk; i += blockDim.x) {
-        const int k = k0 + i;
-        const uint32_t c0w = S(0, k + w), c1w = S(1, k + w), cxw = S(2, k + w), cx1w = S(3, k + w),
-                       cx = S(2, k), cx1 = S(3, k);
-        U[i] = c0w ^ cxw ^ cx ^ cx1;                    // u1
-        U[kToomBlk + i] = c1w ^ cx ^ cx1w ^ cx1;        // u2
-        U[2 * kToomBlk + i] = c0w ^ c1w ^ cxw ^ cx1w;   // u3
-    }
-    __syncthreads();
-    // chains: 3 numerators x w residues, each cut into kToomSeg segments
-    const int per = kToomBlk / w, segl = per / kToomSeg, nthr = 3 * w * kToomSeg;
-    const int t = threadIdx.x;
-    int j = 0, r = 0, sg = 0;
-    if (t < nthr) {
-        j = t / (w * kToomSeg);
-        r = (t / kToomSeg) % w;
-        sg = t % kToomSeg;
-        uint32_t acc = 0;
-        for (int e = sg * segl; e < (sg + 1) * segl; ++e) {
-            const int i = j * kToomBlk + r + e * w;
-            acc ^= U[i];
-            U[i] = acc;
+    // the block as ROWS x w: thread (column r, segment sg) keeps SEGR rows of
+    // u1..u3 and their running prefix in registers; segment carries go
+    // through shared memory
+    constexpr int W = kToomW, ROWS = kToomBlk / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
+    __shared__ uint32_t stot[3][NSEG][W];
+    const int r = int(threadIdx.x) % W, sg = int(threadIdx.x) / W;
+    const int kr = k0 + sg * SEGR * W + r;  // first coefficient of this thread
+    uint32_t v1[SEGR], v2[SEGR], v3[SEGR];
+    {
+        uint32_t a1 = 0, a2 = 0, a3 = 0;
+        uint32_t cx = S(2, kr), cx1 = S(3, kr);
+#pragma unroll
+        for (int i = 0; i < SEGR; ++i) {
+            const int k = kr + i * W;
+            const uint32_t c0w = S(0, k + W), c1w = S(1, k + W), cxw = S(2, k + W), cx1w = S(3, k + W);
+            a1 ^= c0w ^ cxw ^ cx ^ cx1;
+            a2 ^= c1w ^ cx ^ cx1w ^ cx1;
+            a3 ^= c0w ^ c1w ^ cxw ^ cx1w;
+            v1[i] = a1;
+            v2[i] = a2;
+            v3[i] = a3;
+            cx = cxw;
+            cx1 = cx1w;
         }
-        segtot[j][r][sg] = acc;
+        stot[0][sg][r] = a1;
+        stot[1][sg][r] = a2;
+        stot[2][sg][r] = a3;
     }
     __syncthreads();
-    if (t < nthr) {
-        uint32_t carry = 0;
-        for (int s2 = 0; s2 < sg; ++s2) carry ^= segtot[j][r][s2];
-        for (int e = sg * segl; e < (sg + 1) * segl; ++e) U[j * kToomBlk + r + e * w] ^= carry;
+    uint32_t g1 = 0, g2 = 0, g3 = 0;  // carry from the block's earlier segments
+    for (int s2 = 0; s2 < sg; ++s2) {
+        g1 ^= stot[0][s2][r];
+        g2 ^= stot[1][s2][r];
+        g3 ^= stot[2][s2][r];
     }
-    __syncthreads();
     uint32_t *q = Q + item * 5 * int64_t(L);
-    for (int i = threadIdx.x; i < kToomBlk; i += blockDim.x) {
-        const int k = k0 + i;
-        if (k < L) {
-            const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = S(4, k - w) ^ S(4, k - 2 * w);
-            q[k] = c0;
-            q[L + k] = U[i] ^ c0 ^ S(1, k) ^ c4w;          // c1 (no carry)
-            q[2 * L + k] = U[kToomBlk + i] ^ c4 ^ c4w;    // c2 (no carry)
-            q[3 * L + k] = U[2 * kToomBlk + i];           // c3 (no carry)
-            q[4 * L + k] = c4;
+    {
+        uint32_t c4m2 = S(4, kr - 2 * W), c4m1 = S(4, kr - W);
+#pragma unroll
+        for (int i = 0; i < SEGR; ++i) {
+            const int k = kr + i * W;
+            const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = c4m1 ^ c4m2;
+            if (k < L) {
+                q[k] = c0;
+                q[L + k] = v1[i] ^ g1 ^ c0 ^ S(1, k) ^ c4w;  // c1 (no block carry)
+                q[2 * L + k] = v2[i] ^ g2 ^ c4 ^ c4w;       // c2 (no block carry)
+                q[3 * L + k] = v3[i] ^ g3;                  // c3 (no block carry)
+                q[4 * L + k] = c4;
+            }
+            c4m2 = c4m1;
+            c4m1 = c4;
         }
     }
-    if (threadIdx.x < 3 * w) {  // block totals: last element of each chain
-        const int jj = threadIdx.x / w, rr = threadIdx.x % w;
-        Tot[(item * nb + b) * 3 * w + threadIdx.x] = U[jj * kToomBlk + kToomBlk - w + rr];
+    if (sg == NSEG - 1) {  // block totals per chain (the last segment's inclusive values)
+        uint32_t *tt = Tot + (item * nb + b) * 3 * W;
+        tt[r] = v1[SEGR - 1] ^ g1;
+        tt[W + r] = v2[SEGR - 1] ^ g2;
+        tt[2 * W + r] = v3[SEGR - 1] ^ g3;
     }
 }
 
@@ -439,12 +448,48 @@ toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict_
         return v;
     };
     uint32_t *out = R + item * outS;
-    const int kend = min((ob + 1) * kToomBlk, 6 * M);
+    const int kbeg = ob * kToomBlk, kend = min(kbeg + kToomBlk, 6 * M);
     constexpr int NI = kToomBlk / 256;  // outputs per thread, all loads in flight
+    const int a0 = kbeg / M;
+    if (a0 == (kend - 1) / M) {
+        // the whole block lies in [aM, (a+1)M): two fixed streams
+        // R[kk] = c_a[kk - aM] + c_{a-1}[kk - (a-1)M]
+        const int a = a0;
+        const bool ha = a <= 4, hb = a >= 1;
+        const uint32_t *pa = q + (ha ? a : 0) * int64_t(L) - int64_t(a) * M;
+        const uint32_t *pb = q + (hb ? a - 1 : 0) * int64_t(L) - int64_t(a - 1) * M;
+        const uint32_t *ca = carry + (a - 1) * w, *cb = carry + (a - 2) * w;  // per-block stride 3w
+        const bool cra = a >= 1 && a <= 3, crb = a - 1 >= 1 && a - 1 <= 3;
+        uint32_t v[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int kk = kbeg + int(threadIdx.x) + i * 256;
+            uint32_t x = 0;
+            if (kk < kend) {
+                if (ha) {
+                    const int k = kk - a * M;
+                    x ^= __ldg(pa + kk);
+                    if (cra) x ^= ca[(k / kToomBlk) * 3 * w + (k & (w - 1))];
+                }
+                if (hb) {
+                    const int k = kk - (a - 1) * M;
+                    x ^= __ldg(pb + kk);
+                    if (crb) x ^= cb[(k / kToomBlk) * 3 * w + (k & (w - 1))];
+                }
+            }
+            v[i] = x;
+        }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int kk = kbeg + int(threadIdx.x) + i * 256;
+            if (kk < kend) out[kk] = v[i];
+        }
+        return;
+    }
     uint32_t v[NI];
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-        const int kk = ob * kToomBlk + int(threadIdx.x) + i * 256;
+        const int kk = kbeg + int(threadIdx.x) + i * 256;
         const int a = (kk >= M) + (kk >= 2 * M) + (kk >= 3 * M) + (kk >= 4 * M) + (kk >= 5 * M);
         uint32_t x = 0;
         if (kk < kend) {
@@ -455,7 +500,7 @@ toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict_
     }
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-        const int kk = ob * kToomBlk + int(threadIdx.x) + i * 256;
+        const int kk = kbeg + int(threadIdx.x) + i * 256;
         if (kk < kend) out[kk] = v[i];
     }
 }
@@ -1026,7 +1071,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int64_t items = G * ipow5(l - 1), outS = 6 * int64_t(M);
         const int Lin = l == L.tl ? (2 * pl.leaf_words) << pl.levels : int(6 * L.M[l + 1]);
         const int nb = int(ceil_div(2 * M, kToomBlk)), nbo = int(ceil_div(6 * M, kToomBlk));
-        const size_t sms = (size_t(5) * (kToomBlk + 3 * kToomW) + size_t(3) * kToomBlk) * 4;
+        const size_t sms = size_t(5) * (kToomBlk + 3 * kToomW) * 4;
         static int attr_dev_mask = 0;  // benign race: the attribute set is idempotent
         int dev = 0;
         cudaGetDevice(&dev);
