@@ -43,7 +43,8 @@ static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
 static constexpr int kToomW = 16;       // x = X^w (coefficients)
-static constexpr double kToomWordCost = 30.0;  // planner: cost units per word moved (fit on B200)
+static constexpr double kToomWordCost = 24.0;  // planner: cost units per word moved (fit on B200)
+static constexpr int kToomMinWords = 512;      // Toom levels only from t >= 512 words (measured ties below)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -666,7 +667,8 @@ static bool best_leaf(int64_t Smin, int leaf_hint, int &bestLF, int &bestK, doub
         }
         const int KC = std::min(K, kMaxKC);
         if (!find_k2(int(LF), KC)) continue;
-        const double cost = double(ipow3(K)) * double(LF * LF + 48 * LF);
+        // LF >= 37 has 11-quad chunks: 85 KB of shared memory, 2 CTAs/SM (~15 % slower)
+        const double cost = double(ipow3(K)) * double(LF * LF + 48 * LF) * (LF >= 37 ? 1.15 : 1.0);
         if (!bestLF || cost < best) {
             best = cost;
             bestLF = int(LF);
@@ -720,7 +722,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     const int forced = leaf_hint ? 0 : toom_override();
     for (int TL = 0; TL <= kMaxToom; ++TL) {
         if (forced >= 0 && TL != forced) continue;
-        if (TL > 0 && leaf_hint) continue;
+        if (TL > 0 && (leaf_hint || (forced < 0 && t < kToomMinWords))) continue;
         int64_t M[kMaxToom + 1] = {0}, Smin = Nmin;
         if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
         int LF, K;
