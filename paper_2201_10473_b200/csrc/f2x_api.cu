@@ -558,17 +558,19 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
 // stage from contiguous storage runs, then thread i transposes half-word i
 // back to 32 rows and stores its 32-bit halves (adjacent threads = adjacent
 // halves of a row: coalesced).
-__global__ void __launch_bounds__(kTileThreads)
+template <int TW>
+__global__ void __launch_bounds__(2 * TW)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
-    __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
+    constexpr int TC = 64 * TW, TT = 2 * TW;  // coefficients, threads per tile
+    __shared__ uint32_t stage[TC + TC / 32];
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
     const int tile = int(blockIdx.x - g * tiles);
     const uint32_t *Cg = Croot + g * rootStride;
-    const int k0 = tile * kTileCoeffs, kend = min(k0 + kTileCoeffs, 64 * tout);
+    const int k0 = tile * TC, kend = min(k0 + TC, 64 * tout);
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
-    for (int k = k0 + tid; k < k0 + kTileCoeffs; k += kTileThreads)
+    for (int k = k0 + tid; k < k0 + TC; k += TT)
         if (k >= kvalid) stage[stg(k - k0)] = 0u;
     int c, r;
     if (k0 < kvalid) {
@@ -576,9 +578,9 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid, LF, c, r);
         const int s1 = c * LFS + r;
-        StorageWalk w(s0 + tid, k0, LF, LFS);
+        StorageWalkN<TT> w(s0 + tid, k0, LF, LFS);
 #pragma unroll 8
-        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+        for (int sw = s0 + tid; sw < s1; sw += TT) {
             const uint32_t v = __ldg(Cg + sw);  // pads too: loads batch across the unroll
             if (w.data()) stage[stg(w.kk)] = v;
             w.next();
@@ -590,9 +592,9 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
         const int s0 = c * LFS + r;
         chunk_split(kvalid + ncyc, LF, c, r);
         const int s1 = c * LFS + r;
-        StorageWalk w(s0 + tid, k0 + ncyc, LF, LFS);
+        StorageWalkN<TT> w(s0 + tid, k0 + ncyc, LF, LFS);
 #pragma unroll 8
-        for (int sw = s0 + tid; sw < s1; sw += kTileThreads) {
+        for (int sw = s0 + tid; sw < s1; sw += TT) {
             const uint32_t v = __ldg(Cg + sw);
             if (w.data()) stage[stg(w.kk)] ^= v;
             w.next();
@@ -603,7 +605,7 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = stage[stg(32 * tid + i)];
     transpose32(x);
-    const int u = tile * kTileWords + (tid >> 1);
+    const int u = tile * TW + (tid >> 1);
     if (u < tout) {
         const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
         uint32_t *po = reinterpret_cast<uint32_t *>(out) + ((g * 32) * tout + u) * 2 + (tid & 1);
@@ -1096,8 +1098,11 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // K4
     {
         const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
-        const int tiles = int(ceil_div(tout, kTileWords));
-        k4_unslice<<<unsigned(G * tiles), kTileThreads, 0, stream>>>(
+        // 32-word tiles: twice the CTAs of the slicing tiles (the grid is
+        // under one wave at 64 words)
+        constexpr int TW4 = 32;
+        const int tiles = int(ceil_div(tout, TW4));
+        k4_unslice<TW4><<<unsigned(G * tiles), 2 * TW4, 0, stream>>>(
             root, C, batch, tout, rootLF, rootLFS, rootS, ncyc, tiles);
     }
     if ((rc = debug_sync(stream, 4))) return rc;
