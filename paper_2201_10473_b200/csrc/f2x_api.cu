@@ -423,6 +423,135 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     }
 }
 
+// Single-kernel variant: one CTA per item walks its blocks in order, so the
+// chain carries flow from block to block in shared memory and the c_j go
+// straight into R (first contribution to a coefficient written, the second
+// XORed after a barrier): no c_j round trip through HBM, one launch.
+__global__ void __launch_bounds__(kToomScanT)
+toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
+                int Lin, int64_t outS) {
+    extern __shared__ uint32_t tsm[];
+    constexpr int W = kToomW, ROWS = kToomBlk / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
+    constexpr int H = kToomBlk + 3 * W;
+    uint32_t *Stg = tsm;  // [5][H]
+    __shared__ uint32_t stot[3][NSEG][W];
+    __shared__ uint32_t bcar[3][W];  // carry into the current block, per chain
+    const int64_t item = blockIdx.x;
+    const int L = 2 * M, nb = (L + kToomBlk - 1) / kToomBlk;
+    const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
+    uint32_t *Rg = R + item * outS;
+    const bool plain = LFi == LFSi;
+    const int r = int(threadIdx.x) % W, sg = int(threadIdx.x) / W;
+    if (threadIdx.x < 3 * W) bcar[threadIdx.x / W][threadIdx.x % W] = 0u;
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+        const int k0 = b * kToomBlk, kb = k0 - 2 * W;
+        {  // staging: every load of the block in flight at once
+            constexpr int T = kToomScanT, NI = (H + T - 1) / T;
+            uint32_t v[5][NI];
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int h = int(threadIdx.x) + i * T, k = kb + h;
+                    uint32_t x = 0;
+                    if (h < H && k >= 0 && k < Lin) {
+                        int64_t off = k;
+                        if (!plain) {
+                            const int c = __float2int_rz((float(k) + 0.5f) * in.invLF);
+                            off = int64_t(c) * LFSi + (k - c * LFi);
+                        }
+                        x = __ldg(in.C + e * inS + off);
+                    }
+                    v[e][i] = x;
+                }
+            }
+            __syncthreads();  // previous block's readers of Stg / stot are done
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int h = int(threadIdx.x) + i * T;
+                    if (h < H) Stg[e * H + h] = v[e][i];
+                }
+            }
+        }
+        __syncthreads();
+        auto S = [&](int e, int k) -> uint32_t { return Stg[e * H + (k - kb)]; };
+        const int kr = k0 + sg * SEGR * W + r;
+        uint32_t v1[SEGR], v2[SEGR], v3[SEGR];
+        {
+            uint32_t a1 = 0, a2 = 0, a3 = 0;
+            uint32_t cx = S(2, kr), cx1 = S(3, kr);
+#pragma unroll
+            for (int i = 0; i < SEGR; ++i) {
+                const int k = kr + i * W;
+                const uint32_t c0w = S(0, k + W), c1w = S(1, k + W), cxw = S(2, k + W), cx1w = S(3, k + W);
+                a1 ^= c0w ^ cxw ^ cx ^ cx1;
+                a2 ^= c1w ^ cx ^ cx1w ^ cx1;
+                a3 ^= c0w ^ c1w ^ cxw ^ cx1w;
+                v1[i] = a1;
+                v2[i] = a2;
+                v3[i] = a3;
+                cx = cxw;
+                cx1 = cx1w;
+            }
+            stot[0][sg][r] = a1;
+            stot[1][sg][r] = a2;
+            stot[2][sg][r] = a3;
+        }
+        __syncthreads();
+        uint32_t g1 = bcar[0][r], g2 = bcar[1][r], g3 = bcar[2][r];
+        for (int s2 = 0; s2 < sg; ++s2) {
+            g1 ^= stot[0][s2][r];
+            g2 ^= stot[1][s2][r];
+            g3 ^= stot[2][s2][r];
+        }
+        uint32_t c[5][SEGR];
+        {
+            uint32_t c4m2 = S(4, kr - 2 * W), c4m1 = S(4, kr - W);
+#pragma unroll
+            for (int i = 0; i < SEGR; ++i) {
+                const int k = kr + i * W;
+                const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = c4m1 ^ c4m2;
+                c[0][i] = c0;
+                c[1][i] = v1[i] ^ g1 ^ c0 ^ S(1, k) ^ c4w;
+                c[2][i] = v2[i] ^ g2 ^ c4 ^ c4w;
+                c[3][i] = v3[i] ^ g3;
+                c[4][i] = c4;
+                c4m2 = c4m1;
+                c4m1 = c4;
+            }
+        }
+        // R[k + jM]: first contributions (k < M, or j = 4) are plain stores
+#pragma unroll
+        for (int i = 0; i < SEGR; ++i) {
+            const int k = kr + i * W;
+            if (k < L) {
+#pragma unroll
+                for (int j = 0; j < 5; ++j)
+                    if (k < M || j == 4) Rg[k + j * M] = c[j][i];
+            }
+        }
+        __syncthreads();
+        // ... second contributions XOR onto them (written by this CTA, earlier
+        // or before the barrier above)
+#pragma unroll
+        for (int i = 0; i < SEGR; ++i) {
+            const int k = kr + i * W;
+            if (k < L && k >= M) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) Rg[k + j * M] ^= c[j][i];
+            }
+        }
+        if (sg == NSEG - 1) {  // carry into the next block: this block's chain totals
+            bcar[0][r] = v1[SEGR - 1] ^ g1;
+            bcar[1][r] = v2[SEGR - 1] ^ g2;
+            bcar[2][r] = v3[SEGR - 1] ^ g3;
+        }
+    }
+}
+
 // Kernel B: output block ob of item i.  R[k] = c_a[k - aM] + c_{a-1}[k - (a-1)M]
 // (a = k / M), the c_1..c_3 terms plus their chain carries (XOR of the earlier
 // blocks' totals).
@@ -1076,21 +1205,39 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int Lin = l == L.tl ? (2 * pl.leaf_words) << pl.levels : int(6 * L.M[l + 1]);
         const int nb = int(ceil_div(2 * M, kToomBlk)), nbo = int(ceil_div(6 * M, kToomBlk));
         const size_t sms = size_t(5) * (kToomBlk + 3 * kToomW) * 4;
+        // one CTA per item (carries in shared memory) when there are enough
+        // items to fill the GPU, else the two-kernel form (F2X_TOOM_SEQ =
+        // item threshold, experiments)
+        static int seq_min = -1;
+        if (seq_min < 0) {
+            const char *e = getenv("F2X_TOOM_SEQ");
+            seq_min = e ? atoi(e) : 600;  // measured: 640 items seq, 512 two-kernel
+        }
+        const bool seq = items >= seq_min;
         static int attr_dev_mask = 0;  // benign race: the attribute set is idempotent
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 31 && !(attr_dev_mask & (1 << dev))) {
-            const cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        int(sms));
+            cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(sms));
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_interp_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sms));
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             attr_dev_mask |= 1 << dev;
         }
-        toom_interp_scan<<<unsigned(items * nb), kToomScanT, sms, stream>>>(root, Q, Tot, M, kToomW, rootLF, rootLFS,
-                                                                     rootS, Lin, nb);
-        if ((rc = debug_sync(stream, 5))) return rc;
-        const size_t sm = size_t(nb) * 3 * kToomW * 4;
-        toom_interp_assemble<<<unsigned(items * nbo), 256, sm, stream>>>(Q, Tot, out, M, kToomW, nb, nbo, outS);
-        if ((rc = debug_sync(stream, 5))) return rc;
+        if (seq) {
+            toom_interp_seq<<<unsigned(items), kToomScanT, sms, stream>>>(root, out, M, rootLF, rootLFS, rootS,
+                                                                          Lin, outS);
+            if ((rc = debug_sync(stream, 5))) return rc;
+        } else {
+            toom_interp_scan<<<unsigned(items * nb), kToomScanT, sms, stream>>>(root, Q, Tot, M, kToomW, rootLF,
+                                                                                rootLFS, rootS, Lin, nb);
+            if ((rc = debug_sync(stream, 5))) return rc;
+            const size_t sm = size_t(nb) * 3 * kToomW * 4;
+            toom_interp_assemble<<<unsigned(items * nbo), 256, sm, stream>>>(Q, Tot, out, M, kToomW, nb, nbo,
+                                                                             outS);
+            if ((rc = debug_sync(stream, 5))) return rc;
+        }
         root = out;
         rootLF = rootLFS = int(outS);
         rootS = outS;
