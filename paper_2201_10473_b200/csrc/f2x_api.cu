@@ -820,6 +820,18 @@ static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
     Smin_last = M[TL] + 2 * kToomW;
 }
 
+// Toom interpolation: levels with >= this many products use the one-CTA-per-
+// product kernel (F2X_TOOM_SEQ overrides; measured: 640 products sequential,
+// 512 two-kernel)
+static int64_t toom_seq_min() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("F2X_TOOM_SEQ");
+        v = e ? atoll(e) : 600;
+    }
+    return v;
+}
+
 // F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
 static int toom_override() {
     static int v = -2;
@@ -948,12 +960,14 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
     off = align256(L.off_p1 + p1);
-    for (int l = TL; l >= 1; --l) {  // Toom interpolation: block scans, totals, outputs
+    for (int l = TL; l >= 1; --l) {  // Toom interpolation: [block scans, totals,] outputs
         const int64_t items = G * ipow5(l - 1);
-        L.off_q[l] = off;
-        off = align256(off + items * 5 * 2 * L.M[l] * 4);
-        L.off_tot[l] = off;
-        off = align256(off + items * ceil_div(2 * L.M[l], kToomBlk) * 3 * kToomW * 4);
+        L.off_q[l] = L.off_tot[l] = off;
+        if (items < toom_seq_min()) {  // two-kernel form: c_j and chain totals in HBM
+            off = align256(off + items * 5 * 2 * L.M[l] * 4);
+            L.off_tot[l] = off;
+            off = align256(off + items * ceil_div(2 * L.M[l], kToomBlk) * 3 * kToomW * 4);
+        }
         L.off_r[l] = off;
         off = align256(off + items * 6 * L.M[l] * 4);
     }
@@ -1206,14 +1220,8 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int nb = int(ceil_div(2 * M, kToomBlk)), nbo = int(ceil_div(6 * M, kToomBlk));
         const size_t sms = size_t(5) * (kToomBlk + 3 * kToomW) * 4;
         // one CTA per item (carries in shared memory) when there are enough
-        // items to fill the GPU, else the two-kernel form (F2X_TOOM_SEQ =
-        // item threshold, experiments)
-        static int seq_min = -1;
-        if (seq_min < 0) {
-            const char *e = getenv("F2X_TOOM_SEQ");
-            seq_min = e ? atoi(e) : 600;  // measured: 640 items seq, 512 two-kernel
-        }
-        const bool seq = items >= seq_min;
+        // items to fill the GPU, else the two-kernel form
+        const bool seq = items >= toom_seq_min();
         static int attr_dev_mask = 0;  // benign race: the attribute set is idempotent
         int dev = 0;
         cudaGetDevice(&dev);
