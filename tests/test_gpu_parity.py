@@ -359,17 +359,20 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("tl", [0, 1, 2, 3])
-def test_toom_levels_forced(tl, cuda):
+@pytest.mark.parametrize("tl,seq", [(0, None), (1, None), (2, None), (3, None), (2, 1), (2, 10 ** 9)])
+def test_toom_levels_forced(tl, seq, cuda):
     """Toom-3 levels above the Karatsuba node problem (F2X_TOOM, read once per
     process): 0-3 levels give the oracle's bits for ring and full sizes,
-    ragged batches included."""
+    ragged batches included; both interpolation forms (F2X_TOOM_SEQ: one CTA
+    per product for every level / the two-kernel form for every level)."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, F2X_TOOM=str(tl))
+    if seq is not None:
+        env["F2X_TOOM_SEQ"] = str(seq)
     r = subprocess.run([sys.executable, "-c", _TOOM_SCRIPT, root, str(tl)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
