@@ -487,8 +487,14 @@ def extra_configs(torch, np, dev, args, peak) -> dict:
         ms = tot / reps
         t = (n + 63) // 64
         v = batch / (ms / 1e3)
+        from paper_2201_10473_b200.engine import plan as eng_plan
+
+        p = eng_plan("cyclic", batch, n)
         out[f"n{n}"] = {"batch": batch, "ms_per_call": round(ms, 4), "value": round(v, 1),
-                        "whole_call_frac_int_alu": round(v * w_alg(t) / peak["ops_per_s"], 4)}
+                        "whole_call_frac_int_alu": round(v * w_alg(t) / peak["ops_per_s"], 4),
+                        "plan": {"toom_levels": p["toom_levels"], "toom_M": p["toom_M"],
+                                 "leaf_words": p["leaf_words"], "levels": p["levels"],
+                                 "global_levels": p["global_levels"]}}
         del dA, dB, dC
     return out
 
