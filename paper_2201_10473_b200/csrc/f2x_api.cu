@@ -1,9 +1,13 @@
 // Host side of the engine: planner, the C ABI of include/f2x.h, and the
-// three memory-side kernels around the node kernel (f2x_kernels.cuh):
-//   K1 k1_slice      packed uint64[batch][t] -> bitsliced chunked groups
+// memory-side kernels around the node kernel (f2x_kernels.cuh):
+//   K1 k1_slice / k1_slice_eval<EL>
+//                    packed uint64[batch][t] -> bitsliced chunked groups, the
+//                    top EL global Karatsuba levels pre-evaluated
 //                    (+ constant-time top-bit check for ring operands)
+//   toom_eval_level  Toom-3 evaluation, one level (large operands only)
 //   K2 k2_node_mul   per (group, Karatsuba path) node product  [hot kernel]
 //   K3 k3_interp<D>  global Karatsuba interpolation, D levels per pass
+//   toom_interp_*    Toom-3 interpolation, one level (exact divisions)
 //   K4 k4_unslice    fold mod X^n-1 (cyclic) + transpose back to uint64 rows
 // Reference interfaces replaced: schoolbook_mul (poly.py:547-561),
 // clmul64_batch (poly.py:451-480), SPEC ring_mul.
@@ -296,7 +300,6 @@ toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb
 // (B) per block of outputs, the carries (XOR of earlier blocks' totals) and
 // the assembly of R from two c_j terms per coefficient.
 constexpr int kToomBlk = 2048;   // coefficients per block (multiple of w)
-constexpr int kToomSeg = 4;      // scan segments per chain and block (3 w kToomSeg <= threads)
 constexpr int kToomScanT = 256;  // threads of the scan kernel
 
 struct ToomIn {
