@@ -34,6 +34,29 @@ def _workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> 
         return ws
 
 
+# Scratch budget per call: larger batches run as consecutive row chunks (whole
+# 32-row groups) on the same stream, so memory stays bounded; F2X_WS_BUDGET
+# (bytes) overrides the default of 8 GiB.
+_WS_BUDGET = int(__import__("os").environ.get("F2X_WS_BUDGET", str(8 << 30)))
+
+
+def _row_chunks(lib, kind: int, batch: int, t_or_n: int, leaf: int) -> tuple[list, int]:
+    """[(lo, hi), ...] row ranges whose workspace fits the budget, and the
+    largest workspace among them."""
+    need = int(lib.f2x_workspace_bytes(kind, batch, t_or_n, leaf))
+    if need < 0:
+        _lib.check(need, "f2x_workspace_bytes")
+    if need <= _WS_BUDGET or batch <= 32:
+        return [(0, batch)], need
+    groups = -(-batch // 32)
+    per = max(1, int(groups * _WS_BUDGET // need))  # workspace is ~linear in groups
+    while per > 1 and int(lib.f2x_workspace_bytes(kind, 32 * per, t_or_n, leaf)) > _WS_BUDGET:
+        per = max(1, per * 7 // 8)
+    rows = 32 * per
+    chunks = [(lo, min(lo + rows, batch)) for lo in range(0, batch, rows)]
+    return chunks, int(lib.f2x_workspace_bytes(kind, rows, t_or_n, leaf))
+
+
 def _check_operands(A: torch.Tensor, B: torch.Tensor) -> None:
     if not isinstance(A, torch.Tensor) or not isinstance(B, torch.Tensor):
         raise TypeError("operands must be torch tensors")
@@ -71,13 +94,12 @@ def mul_full(A: torch.Tensor, B: torch.Tensor, *, out: torch.Tensor | None = Non
     lib = _lib.load()
     with torch.cuda.device(A.device):
         stream = torch.cuda.current_stream(A.device)
-        need = lib.f2x_workspace_bytes(_lib.KIND_FULL, batch, t, leaf)
-        if need < 0:
-            _lib.check(int(need), "f2x_workspace_bytes")
+        chunks, need = _row_chunks(lib, _lib.KIND_FULL, batch, t, leaf)
         ws = _workspace(A.device, stream, need)
-        rc = lib.f2x_mul_full(A.data_ptr(), B.data_ptr(), out.data_ptr(), batch, t,
-                              ws.data_ptr(), ws.numel(), leaf, stream.cuda_stream)
-    _lib.check(rc, "f2x_mul_full")
+        for lo, hi in chunks:
+            rc = lib.f2x_mul_full(A[lo:hi].data_ptr(), B[lo:hi].data_ptr(), out[lo:hi].data_ptr(),
+                                  hi - lo, t, ws.data_ptr(), ws.numel(), leaf, stream.cuda_stream)
+            _lib.check(rc, "f2x_mul_full")
     return out
 
 
@@ -113,14 +135,13 @@ def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | 
         flag = err_flag
         if flag is None:
             flag = torch.zeros(1, dtype=torch.int32, device=A.device)
-        need = lib.f2x_workspace_bytes(_lib.KIND_CYCLIC, batch, n, leaf)
-        if need < 0:
-            _lib.check(int(need), "f2x_workspace_bytes")
+        chunks, need = _row_chunks(lib, _lib.KIND_CYCLIC, batch, n, leaf)
         ws = _workspace(A.device, stream, need)
-        rc = lib.f2x_mul_cyclic(A.data_ptr(), B.data_ptr(), out.data_ptr(), batch, n,
-                                ws.data_ptr(), ws.numel(), leaf, flag.data_ptr(),
-                                stream.cuda_stream)
-    _lib.check(rc, "f2x_mul_cyclic")
+        for lo, hi in chunks:
+            rc = lib.f2x_mul_cyclic(A[lo:hi].data_ptr(), B[lo:hi].data_ptr(), out[lo:hi].data_ptr(),
+                                    hi - lo, n, ws.data_ptr(), ws.numel(), leaf, flag.data_ptr(),
+                                    stream.cuda_stream)
+            _lib.check(rc, "f2x_mul_cyclic")
     if check and err_flag is None and int(flag.item()) != 0:
         raise ValueError("operand has bits set at or above n")
     return out

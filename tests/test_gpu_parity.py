@@ -376,3 +376,33 @@ def test_toom_levels_forced(tl, seq, cuda):
     r = subprocess.run([sys.executable, "-c", _TOOM_SCRIPT, root, str(tl)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_workspace_budget_row_chunks(cuda):
+    """A small scratch budget (F2X_WS_BUDGET, read at import) splits the batch
+    into row chunks; results stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import c_mul_cyclic, c_mul_full
+from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+from paper_2201_10473_b200 import engine, mul_cyclic, mul_full
+from paper_2201_10473_b200 import _lib
+dev = torch.device("cuda", 0)
+d = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)
+A, B = make_cyclic_inputs(17669, 1000)
+assert len(engine._row_chunks(_lib.load(), _lib.KIND_CYCLIC, 1000, 17669, 0)[0]) > 3
+assert np.array_equal(mul_cyclic(d(A), d(B), 17669).cpu().numpy().view(np.uint64), c_mul_cyclic(A, B, 17669))
+A, B = make_full_inputs(64, 700, words=True)
+assert np.array_equal(mul_full(d(A), d(B)).cpu().numpy().view(np.uint64), c_mul_full(A, B))
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, F2X_WS_BUDGET=str(8 << 20))
+    r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

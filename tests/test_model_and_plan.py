@@ -343,3 +343,20 @@ def test_toom_plan_sizes(kind, size, tl):
         Ms = p["toom_M"]
         assert 3 * Ms[0] >= 64 * t and len(Ms) == p["toom_levels"]
         assert p["leaf_words"] << p["levels"] >= Ms[-1] + 2 * p["toom_w"]
+
+
+def test_row_chunks_bound_workspace(monkeypatch):
+    """Batches whose scratch exceeds the budget run as whole-group row
+    chunks, each within the budget, covering every row once."""
+    from paper_2201_10473_b200 import _lib, engine
+
+    lib = _lib.load()
+    full = int(lib.f2x_workspace_bytes(_lib.KIND_CYCLIC, 100_000, 17669, 0))
+    monkeypatch.setattr(engine, "_WS_BUDGET", full // 7)
+    chunks, need = engine._row_chunks(lib, _lib.KIND_CYCLIC, 100_000, 17669, 0)
+    assert len(chunks) >= 7 and need <= full // 7
+    assert chunks[0][0] == 0 and chunks[-1][1] == 100_000
+    for (a, b), (c, _) in zip(chunks, chunks[1:]):
+        assert b == c and (b - a) % 32 == 0
+    monkeypatch.setattr(engine, "_WS_BUDGET", 8 << 30)
+    assert engine._row_chunks(lib, _lib.KIND_CYCLIC, 4096, 17669, 0)[0] == [(0, 4096)]
