@@ -12,6 +12,7 @@
 // Reference interfaces replaced: schoolbook_mul (poly.py:547-561),
 // clmul64_batch (poly.py:451-480), SPEC ring_mul.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -768,11 +769,10 @@ struct Layout {
 // 2 where the parts are whole operand words; F2X_EVAL_LEVELS=0/1/2 overrides
 // (experiments).
 static int eval_levels_for(int GL, int64_t N) {
-    static int v = -2;
-    if (v == -2) {
+    static const int v = [] {  // thread-safe one-time read
         const char *e = getenv("F2X_EVAL_LEVELS");
-        v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : -1;
-    }
+        return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : -1;
+    }();
     // default 2: measured +1.3% (n=17669), +2.6% (35851), +1.8% (57637)
     int el = v >= 0 ? v : 2;
     if (el > GL) el = GL;
@@ -827,21 +827,19 @@ static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
 // product kernel (F2X_TOOM_SEQ overrides; measured: 640 products sequential,
 // 512 two-kernel)
 static int64_t toom_seq_min() {
-    static int64_t v = -1;
-    if (v < 0) {
+    static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
-        v = e ? atoll(e) : 600;
-    }
+        return e ? int64_t(atoll(e)) : int64_t(600);
+    }();
     return v;
 }
 
 // F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
 static int toom_override() {
-    static int v = -2;
-    if (v == -2) {
+    static const int v = [] {
         const char *e = getenv("F2X_TOOM");
-        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : -1;
-    }
+        return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : -1;
+    }();
     return v;
 }
 
@@ -1028,11 +1026,10 @@ __global__ void __launch_bounds__(256) lop3_peak(uint32_t *out, int iters, uint3
 // F2X_DEBUG_SYNC=1: synchronise after every launch and report the failing
 // stage (development aid; never set in benchmarks).
 static int debug_sync(cudaStream_t s, int stage) {
-    static int enabled = -1;
-    if (enabled < 0) {
+    static const bool enabled = [] {
         const char *v = getenv("F2X_DEBUG_SYNC");
-        enabled = v && v[0] == '1';
-    }
+        return v && v[0] == '1';
+    }();
     if (!enabled) return 0;
     cudaError_t e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -1115,15 +1112,15 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         dim3 grid(unsigned(G * tiles), 2);
         const size_t sm = size_t(1 << L.el) * (64 * TW + 2 * TW) * 4;
         const size_t sm_max = size_t(1 << L.el) * (64 * kTileWords + 2 * kTileWords) * 4;
-        static int attr_dev_mask[3] = {0, 0, 0};  // benign race: the attribute set is idempotent
+        static std::atomic<uint32_t> attr_dev_mask[3];  // per EL: devices configured
         int dev = 0;
         cudaGetDevice(&dev);
-        if (dev < 31 && !(attr_dev_mask[L.el] & (1 << dev))) {
+        if (dev < 31 && !(attr_dev_mask[L.el].load() & (1u << dev))) {
             const cudaError_t ae = L.el == 1
                 ? cudaFuncSetAttribute(k1_slice_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max))
                 : cudaFuncSetAttribute(k1_slice_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max));
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
-            attr_dev_mask[L.el] |= 1 << dev;
+            attr_dev_mask[L.el].fetch_or(1u << dev);
         }
         if (L.el == 1) {
             k1_slice_eval<1><<<grid, kTileThreads << 1, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
@@ -1225,16 +1222,16 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         // one CTA per item (carries in shared memory) when there are enough
         // items to fill the GPU, else the two-kernel form
         const bool seq = items >= toom_seq_min();
-        static int attr_dev_mask = 0;  // benign race: the attribute set is idempotent
+        static std::atomic<uint32_t> attr_dev_mask{0};  // devices configured (idempotent set)
         int dev = 0;
         cudaGetDevice(&dev);
-        if (dev < 31 && !(attr_dev_mask & (1 << dev))) {
+        if (dev < 31 && !(attr_dev_mask.load() & (1u << dev))) {
             cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sms));
             if (ae == cudaSuccess)
                 ae = cudaFuncSetAttribute(toom_interp_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sms));
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
-            attr_dev_mask |= 1 << dev;
+            attr_dev_mask.fetch_or(1u << dev);
         }
         if (seq) {
             toom_interp_seq<<<unsigned(items), kToomScanT, sms, stream>>>(root, out, M, rootLF, rootLFS, rootS,
