@@ -48,8 +48,8 @@ static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
 static constexpr int kToomW = 16;       // x = X^w (coefficients)
-static constexpr double kToomWordCost = 24.0;  // planner: cost units per word moved (fit on B200)
-static constexpr int kToomMinWords = 512;      // Toom levels only from t >= 512 words (measured ties below)
+static constexpr double kToomWordCost = 15.0;  // planner: cost units per word moved (fit on B200)
+static constexpr int kToomMinWords = 544;      // Toom only above 512 words: d=32768 (t=512) measured 4.6 % slower with it
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -431,7 +431,7 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
 // XORed after a barrier): no c_j round trip through HBM, one launch.
-__global__ void __launch_bounds__(kToomScanT)
+__global__ void __launch_bounds__(kToomScanT, 4)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS) {
     extern __shared__ uint32_t tsm[];
@@ -511,22 +511,20 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             g2 ^= stot[1][s2][r];
             g3 ^= stot[2][s2][r];
         }
-        uint32_t c[5][SEGR];
-        {
-            uint32_t c4m2 = S(4, kr - 2 * W), c4m1 = S(4, kr - W);
-#pragma unroll
-            for (int i = 0; i < SEGR; ++i) {
-                const int k = kr + i * W;
-                const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = c4m1 ^ c4m2;
-                c[0][i] = c0;
-                c[1][i] = v1[i] ^ g1 ^ c0 ^ S(1, k) ^ c4w;
-                c[2][i] = v2[i] ^ g2 ^ c4 ^ c4w;
-                c[3][i] = v3[i] ^ g3;
-                c[4][i] = c4;
-                c4m2 = c4m1;
-                c4m1 = c4;
+        // c_j of this thread's rows, recomputed from the scans and the staged
+        // inputs for each of the two store phases (fewer live registers:
+        // 4 CTAs/SM instead of 3)
+        auto cval = [&](int i, int j) -> uint32_t {
+            const int k = kr + i * W;
+            const uint32_t c4w = S(4, k - W) ^ S(4, k - 2 * W);
+            switch (j) {
+                case 0: return S(0, k);
+                case 1: return v1[i] ^ g1 ^ S(0, k) ^ S(1, k) ^ c4w;
+                case 2: return v2[i] ^ g2 ^ S(4, k) ^ c4w;
+                case 3: return v3[i] ^ g3;
+                default: return S(4, k);
             }
-        }
+        };
         // R[k + jM]: first contributions (k < M, or j = 4) are plain stores
 #pragma unroll
         for (int i = 0; i < SEGR; ++i) {
@@ -534,7 +532,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             if (k < L) {
 #pragma unroll
                 for (int j = 0; j < 5; ++j)
-                    if (k < M || j == 4) Rg[k + j * M] = c[j][i];
+                    if (k < M || j == 4) Rg[k + j * M] = cval(i, j);
             }
         }
         __syncthreads();
@@ -545,7 +543,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             const int k = kr + i * W;
             if (k < L && k >= M) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) Rg[k + j * M] ^= c[j][i];
+                for (int j = 0; j < 4; ++j) Rg[k + j * M] ^= cval(i, j);
             }
         }
         if (sg == NSEG - 1) {  // carry into the next block: this block's chain totals
