@@ -302,6 +302,10 @@ toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb
 // the assembly of R from two c_j terms per coefficient.
 constexpr int kToomBlk = 2048;   // coefficients per block (multiple of w)
 constexpr int kToomScanT = 256;  // threads of the scan kernel
+// staging index: 16 pad words per 128, so the two half-warps of a row scan
+// (rows 8 apart = 128 words) hit different banks
+__device__ __forceinline__ int tstg(int h) { return h + 16 * (h >> 7); }
+constexpr int kToomStgStride = (kToomBlk + 3 * kToomW) + 16 * (((kToomBlk + 3 * kToomW) >> 7) + 1);
 
 struct ToomIn {
     const uint32_t *C;  // item base (5 products)
@@ -327,6 +331,7 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
                  int w, int LFi, int LFSi, int64_t inS, int Lin, int nb) {
     extern __shared__ uint32_t tsm[];
     const int H = kToomBlk + 3 * w;          // staged span per input
+    constexpr int HP = kToomStgStride;        // padded stride per input (see tstg)
     uint32_t *Stg = tsm;                      // [5][H], index k - (k0 - 2w)
     const int64_t item = blockIdx.x / nb;
     const int b = int(blockIdx.x - item * nb);
@@ -360,12 +365,12 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const int h = int(threadIdx.x) + i * T;
-                if (h < H) Stg[e * H + h] = v[e][i];
+                if (h < H) Stg[e * HP + tstg(h)] = v[e][i];
             }
         }
     }
     __syncthreads();
-    auto S = [&](int e, int k) -> uint32_t { return Stg[e * H + (k - kb)]; };
+    auto S = [&](int e, int k) -> uint32_t { return Stg[e * HP + tstg(k - kb)]; };
     // the block as ROWS x w: thread (column r, segment sg) keeps SEGR rows of
     // u1..u3 and their running prefix in registers; segment carries go
     // through shared memory
@@ -437,7 +442,8 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
     extern __shared__ uint32_t tsm[];
     constexpr int W = kToomW, ROWS = kToomBlk / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
     constexpr int H = kToomBlk + 3 * W;
-    uint32_t *Stg = tsm;  // [5][H]
+    constexpr int HP = kToomStgStride;  // padded stride per input (see tstg)
+    uint32_t *Stg = tsm;  // [5][HP]
     __shared__ uint32_t stot[3][NSEG][W];
     __shared__ uint32_t bcar[3][W];  // carry into the current block, per chain
     const int64_t item = blockIdx.x;
@@ -476,12 +482,12 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
                     const int h = int(threadIdx.x) + i * T;
-                    if (h < H) Stg[e * H + h] = v[e][i];
+                    if (h < H) Stg[e * HP + tstg(h)] = v[e][i];
                 }
             }
         }
         __syncthreads();
-        auto S = [&](int e, int k) -> uint32_t { return Stg[e * H + (k - kb)]; };
+        auto S = [&](int e, int k) -> uint32_t { return Stg[e * HP + tstg(k - kb)]; };
         const int kr = k0 + sg * SEGR * W + r;
         uint32_t v1[SEGR], v2[SEGR], v3[SEGR];
         {
@@ -538,12 +544,24 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         __syncthreads();
         // ... second contributions XOR onto them (written by this CTA, earlier
         // or before the barrier above)
+        // (loads of a half batch first: the stores cannot be reordered above
+        // them by the compiler, so one latency per half instead of per word)
 #pragma unroll
-        for (int i = 0; i < SEGR; ++i) {
-            const int k = kr + i * W;
-            if (k < L && k >= M) {
+        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 2) {
+            uint32_t old[SEGR / 2][4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) Rg[k + j * M] ^= cval(i, j);
+            for (int i = 0; i < SEGR / 2; ++i) {
+                const int k = kr + (h2 + i) * W;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) old[i][j] = (k < L && k >= M) ? Rg[k + j * M] : 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < SEGR / 2; ++i) {
+                const int k = kr + (h2 + i) * W;
+                if (k < L && k >= M) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ cval(h2 + i, j);
+                }
             }
         }
         if (sg == NSEG - 1) {  // carry into the next block: this block's chain totals
@@ -1216,7 +1234,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int64_t items = G * ipow5(l - 1), outS = 6 * int64_t(M);
         const int Lin = l == L.tl ? (2 * pl.leaf_words) << pl.levels : int(6 * L.M[l + 1]);
         const int nb = int(ceil_div(2 * M, kToomBlk)), nbo = int(ceil_div(6 * M, kToomBlk));
-        const size_t sms = size_t(5) * (kToomBlk + 3 * kToomW) * 4;
+        const size_t sms = size_t(5) * kToomStgStride * 4;
         // one CTA per item (carries in shared memory) when there are enough
         // items to fill the GPU, else the two-kernel form
         const bool seq = items >= toom_seq_min();
