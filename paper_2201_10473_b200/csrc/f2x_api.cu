@@ -547,16 +547,16 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         // (loads of a half batch first: the stores cannot be reordered above
         // them by the compiler, so one latency per half instead of per word)
 #pragma unroll
-        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 2) {
-            uint32_t old[SEGR / 2][4];
+        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 4) {
+            uint32_t old[SEGR / 4][4];
 #pragma unroll
-            for (int i = 0; i < SEGR / 2; ++i) {
+            for (int i = 0; i < SEGR / 4; ++i) {
                 const int k = kr + (h2 + i) * W;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) old[i][j] = (k < L && k >= M) ? Rg[k + j * M] : 0u;
             }
 #pragma unroll
-            for (int i = 0; i < SEGR / 2; ++i) {
+            for (int i = 0; i < SEGR / 4; ++i) {
                 const int k = kr + (h2 + i) * W;
                 if (k < L && k >= M) {
 #pragma unroll
