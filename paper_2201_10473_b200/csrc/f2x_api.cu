@@ -840,12 +840,12 @@ static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
 }
 
 // Toom interpolation: levels with >= this many products use the one-CTA-per-
-// product kernel (F2X_TOOM_SEQ overrides; measured: 640 products sequential,
-// 512 two-kernel)
+// product kernel (F2X_TOOM_SEQ overrides; measured: 512 products sequential
+// (n=57637 level 1: 263 vs 389 us), 128 two-kernel (n=35851 level 1))
 static int64_t toom_seq_min() {
     static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
-        return e ? int64_t(atoll(e)) : int64_t(600);
+        return e ? int64_t(atoll(e)) : int64_t(256);
     }();
     return v;
 }
