@@ -406,3 +406,15 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("t", [2048, 4096, 8192])
+def test_large_full_sizes_vs_oracle(t, cuda):
+    """Beyond the d-sweep (131k-524k bits): Toom-3 plans with deep Karatsuba
+    node problems stay bit-exact."""
+    from oracle import c_mul_full
+    from oracle.f2x_oracle import make_full_inputs
+    from paper_2201_10473_b200 import mul_full
+
+    A, B = make_full_inputs(t, 33, words=True)
+    assert np.array_equal(_np(mul_full(_dev(A, cuda), _dev(B, cuda))), c_mul_full(A, B))
