@@ -418,3 +418,27 @@ def test_large_full_sizes_vs_oracle(t, cuda):
 
     A, B = make_full_inputs(t, 33, words=True)
     assert np.array_equal(_np(mul_full(_dev(A, cuda), _dev(B, cuda))), c_mul_full(A, B))
+
+
+def test_integration_stub_runs(cuda):
+    """The ctypes binding shown in INTEGRATION.md §2 (what a reference
+    maintainer would add as f2xmul/gpu.py) runs as written against this
+    build and gives the oracle's bits."""
+    import os
+    import re
+
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200 import _lib
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# f2xmul/gpu.py.*?)```", text, re.S).group(1)
+    code = code.replace("from .poly import PolyWords, WideProduct\n", "")
+    code = code.replace('ctypes.CDLL("libf2x.so")', f'ctypes.CDLL("{_lib.LIB_PATH}")')
+    ns: dict = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    A, B = make_full_inputs(64, 40, words=True)
+    assert np.array_equal(ns["schoolbook_mul_batch"](A, B), c_mul_full(A, B))
+    A, B = make_cyclic_inputs(17669, 40)
+    assert np.array_equal(ns["ring_mul_batch"](A, B, 17669), c_mul_cyclic(A, B, 17669))
