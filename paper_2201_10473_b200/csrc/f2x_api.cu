@@ -436,7 +436,7 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
 // XORed after a barrier): no c_j round trip through HBM, one launch.
-__global__ void __launch_bounds__(kToomScanT, 4)
+__global__ void __launch_bounds__(kToomScanT, 3)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS) {
     extern __shared__ uint32_t tsm[];
@@ -517,50 +517,49 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             g2 ^= stot[1][s2][r];
             g3 ^= stot[2][s2][r];
         }
-        // c_j of this thread's rows, recomputed from the scans and the staged
-        // inputs for each of the two store phases (fewer live registers:
-        // 4 CTAs/SM instead of 3)
-        auto cval = [&](int i, int j) -> uint32_t {
-            const int k = kr + i * W;
-            const uint32_t c4w = S(4, k - W) ^ S(4, k - 2 * W);
-            switch (j) {
-                case 0: return S(0, k);
-                case 1: return v1[i] ^ g1 ^ S(0, k) ^ S(1, k) ^ c4w;
-                case 2: return v2[i] ^ g2 ^ S(4, k) ^ c4w;
-                case 3: return v3[i] ^ g3;
-                default: return S(4, k);
-            }
-        };
-        // R[k + jM]: first contributions (k < M, or j = 4) are plain stores
+        // c_0..c_4 of each row once: first contributions to R[k + jM] (k < M,
+        // or j = 4) are plain stores; c_0..c_3 of rows with k >= M are kept
+        // in registers for the read-modify-write after the barrier
+        uint32_t keep[SEGR][4];
+        {
+            uint32_t c4m2 = S(4, kr - 2 * W), c4m1 = S(4, kr - W);
 #pragma unroll
-        for (int i = 0; i < SEGR; ++i) {
-            const int k = kr + i * W;
-            if (k < L) {
+            for (int i = 0; i < SEGR; ++i) {
+                const int k = kr + i * W;
+                const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = c4m1 ^ c4m2;
+                const uint32_t cj[5] = {c0, v1[i] ^ g1 ^ c0 ^ S(1, k) ^ c4w, v2[i] ^ g2 ^ c4 ^ c4w, v3[i] ^ g3, c4};
+                if (k < L) {
+                    if (k < M) {
 #pragma unroll
-                for (int j = 0; j < 5; ++j)
-                    if (k < M || j == 4) Rg[k + j * M] = cval(i, j);
+                        for (int j = 0; j < 5; ++j) Rg[k + j * M] = cj[j];
+                    } else {
+                        Rg[k + 4 * M] = c4;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) keep[i][j] = cj[j];
+                c4m2 = c4m1;
+                c4m1 = c4;
             }
         }
         __syncthreads();
         // ... second contributions XOR onto them (written by this CTA, earlier
-        // or before the barrier above)
-        // (loads of a half batch first: the stores cannot be reordered above
-        // them by the compiler, so one latency per half instead of per word)
+        // or before the barrier above); loads of a half batch first
 #pragma unroll
-        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 4) {
-            uint32_t old[SEGR / 4][4];
+        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 2) {
+            uint32_t old[SEGR / 2][4];
 #pragma unroll
-            for (int i = 0; i < SEGR / 4; ++i) {
+            for (int i = 0; i < SEGR / 2; ++i) {
                 const int k = kr + (h2 + i) * W;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) old[i][j] = (k < L && k >= M) ? Rg[k + j * M] : 0u;
             }
 #pragma unroll
-            for (int i = 0; i < SEGR / 4; ++i) {
+            for (int i = 0; i < SEGR / 2; ++i) {
                 const int k = kr + (h2 + i) * W;
                 if (k < L && k >= M) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ cval(h2 + i, j);
+                    for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ keep[h2 + i][j];
                 }
             }
         }
