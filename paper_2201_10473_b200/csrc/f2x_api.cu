@@ -451,12 +451,38 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
     const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
     uint32_t *Rg = R + item * outS;
     const bool plain = LFi == LFSi;
+    // quad staging: plain inputs whose item/row offsets and length are whole
+    // quads (block starts are multiples of 4: kToomBlk and 2w are)
+    const bool vec = plain && (inS % 4) == 0 && (Lin % 4) == 0 &&
+                     (reinterpret_cast<uintptr_t>(Cin) & 15) == 0;
     const int r = int(threadIdx.x) % W, sg = int(threadIdx.x) / W;
     if (threadIdx.x < 3 * W) bcar[threadIdx.x / W][threadIdx.x % W] = 0u;
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
         const int k0 = b * kToomBlk, kb = k0 - 2 * W;
-        {  // staging: every load of the block in flight at once
+        if (vec) {  // plain, 16-byte aligned inputs: quads, all in flight per half
+            constexpr int T = kToomScanT, H4 = H / 4, NQ = (5 * H4 + T - 1) / T, NH = (NQ + 1) / 2;
+            __syncthreads();  // previous block's readers of Stg / stot are done
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint4 q4[NH];
+#pragma unroll
+                for (int i = 0; i < NH; ++i) {
+                    const int x = int(threadIdx.x) + (half * NH + i) * T;
+                    const int e = x / H4, hq = x - e * H4, k = kb + 4 * hq;
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (x < 5 * H4 && k >= 0 && k < Lin)  // Lin % 4 == 0: whole quads
+                        v = __ldg(reinterpret_cast<const uint4 *>(in.C + e * inS + k));
+                    q4[i] = v;
+                }
+#pragma unroll
+                for (int i = 0; i < NH; ++i) {
+                    const int x = int(threadIdx.x) + (half * NH + i) * T;
+                    const int e = x / H4, hq = x - e * H4;
+                    if (x < 5 * H4) *reinterpret_cast<uint4 *>(Stg + e * HP + tstg(4 * hq)) = q4[i];
+                }
+            }
+        } else         {  // staging: every load of the block in flight at once
             constexpr int T = kToomScanT, NI = (H + T - 1) / T;
             uint32_t v[5][NI];
 #pragma unroll
