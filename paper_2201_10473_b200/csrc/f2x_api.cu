@@ -58,6 +58,8 @@ static inline int64_t ipow5(int k) {
     while (k-- > 0) r *= 5;
     return r;
 }
+// row stride of a plain Toom operand of 3M coefficients: whole 16-byte quads
+static inline int64_t toom_opstride(int64_t M) { return (3 * M + 3) / 4 * 4; }
 static inline int64_t ipow3(int k) {
     int64_t r = 1;
     while (k-- > 0) r *= 3;
@@ -284,6 +286,60 @@ toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb
     y[2 * outS] = a0 ^ xs;
     y[3 * outS] = p1 ^ xs;
     y[4 * outS] = a2;
+}
+
+// Quad form of toom_eval_level (outS and LFSo multiples of 4, 16-byte
+// aligned outputs): grid (output quads / 256, input items, operand), one
+// output storage QUAD per thread -- no 64-bit index division, one chunk
+// split per quad (a quad never straddles a chunk), 16-byte stores.  The
+// per-word form was issue-bound (72-78 % issue slots at n=57637).
+__global__ void __launch_bounds__(256)
+toom_eval_level_q(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
+                  uint32_t *__restrict__ Yb, int64_t inS, int M, int w, int S, int LFo, int LFSo, int64_t outS) {
+    const int sq = int(blockIdx.x) * 256 + int(threadIdx.x);
+    const int sw0 = 4 * sq;
+    if (sw0 >= outS) return;
+    const int64_t i = blockIdx.y;
+    int k0, r0, lim;
+    if (LFo == LFSo) {
+        k0 = sw0;
+        r0 = 0;
+        lim = 4;
+    } else {
+        const int c = sw0 / LFSo;
+        r0 = sw0 - c * LFSo;
+        k0 = c * LFo + r0;
+        lim = LFo - r0;  // words r < lim of the quad hold data
+    }
+    const uint32_t *x = (blockIdx.z ? Xb : Xa) + i * inS;
+    uint32_t y0[4], y1[4], y2[4], y3[4], y4[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int k = k0 + r;
+        uint32_t a0 = 0, a1 = 0, a2 = 0, s1 = 0, s2 = 0;
+        if (r < lim && k < S) {
+            if (k < M) {
+                a0 = __ldg(x + k);
+                a1 = __ldg(x + M + k);
+                a2 = __ldg(x + 2 * M + k);
+            }
+            if (k >= w && k - w < M) s1 = __ldg(x + M + k - w);
+            if (k >= 2 * w && k - 2 * w < M) s2 = __ldg(x + 2 * M + k - 2 * w);
+        }
+        const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
+        y0[r] = a0;
+        y1[r] = p1;
+        y2[r] = a0 ^ xs;
+        y3[r] = p1 ^ xs;
+        y4[r] = a2;
+    }
+    uint4 *y = reinterpret_cast<uint4 *>((blockIdx.z ? Yb : Ya) + i * 5 * outS + sw0);
+    const int64_t o4 = outS / 4;
+    y[0] = make_uint4(y0[0], y0[1], y0[2], y0[3]);
+    y[o4] = make_uint4(y1[0], y1[1], y1[2], y1[3]);
+    y[2 * o4] = make_uint4(y2[0], y2[1], y2[2], y2[3]);
+    y[3 * o4] = make_uint4(y3[0], y3[1], y3[2], y3[3]);
+    y[4 * o4] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
 }
 
 // One Toom-3 interpolation level, from the 5 products C_e of every output
@@ -987,7 +1043,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         off = align256(off + 2 * G * 3 * L.M[1] * 4);
         for (int l = 1; l < TL; ++l) {
             L.off_x[l] = off;
-            off = align256(off + 2 * G * ipow5(l) * 3 * L.M[l + 1] * 4);
+            off = align256(off + 2 * G * ipow5(l) * toom_opstride(L.M[l + 1]) * 4);
         }
     }
     const int64_t opw = G2 * ipow3(L.el) * (L.Ns >> L.el);  // node-problem operand words
@@ -1115,7 +1171,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         // operands (LF 2^K coefficients)
         for (int l = 1; l <= L.tl; ++l) {
             const uint32_t *xa = reinterpret_cast<const uint32_t *>(w + L.off_x[l - 1]);
-            const int64_t items_in = G * ipow5(l - 1), inS = 3 * L.M[l];
+            const int64_t items_in = G * ipow5(l - 1), inS = l == 1 ? 3 * L.M[1] : toom_opstride(L.M[l]);
             const uint32_t *xb = xa + items_in * inS;
             uint32_t *ya, *yb;
             int S, LFo, LFSo;
@@ -1124,7 +1180,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                 ya = reinterpret_cast<uint32_t *>(w + L.off_x[l]);
                 S = int(3 * L.M[l + 1]);
                 LFo = LFSo = S;
-                outS = S;
+                outS = toom_opstride(L.M[l + 1]);  // whole quads; pad words written 0
                 yb = ya + items_in * 5 * outS;
             } else {
                 ya = Abs;
@@ -1134,9 +1190,15 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                 LFSo = pl.leaf_stride;
                 outS = L.Ns;
             }
-            dim3 grid(unsigned(ceil_div(items_in * outS, 256)), 2);
-            toom_eval_level<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
-                                                      S, LFo, LFSo, outS);
+            if (outS % 4 == 0 && (LFo == LFSo || LFSo % 4 == 0) && items_in <= 65535) {
+                dim3 grid(unsigned(ceil_div(outS / 4, 256)), unsigned(items_in), 2);
+                toom_eval_level_q<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, inS, int(L.M[l]), kToomW, S, LFo,
+                                                            LFSo, outS);
+            } else {
+                dim3 grid(unsigned(ceil_div(items_in * outS, 256)), 2);
+                toom_eval_level<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
+                                                          S, LFo, LFSo, outS);
+            }
             if ((rc = debug_sync(stream, 1))) return rc;
         }
     } else if (L.el == 0) {
