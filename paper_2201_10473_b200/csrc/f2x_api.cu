@@ -361,7 +361,10 @@ constexpr int kToomScanT = 256;  // threads of the scan kernel
 // staging index: 16 pad words per 128, so the two half-warps of a row scan
 // (rows 8 apart = 128 words) hit different banks
 __device__ __forceinline__ int tstg(int h) { return h + 16 * (h >> 7); }
-constexpr int kToomStgStride = (kToomBlk + 3 * kToomW) + 16 * (((kToomBlk + 3 * kToomW) >> 7) + 1);
+__host__ __device__ constexpr int toom_stg_stride(int blk) {
+    return (blk + 3 * kToomW) + 16 * (((blk + 3 * kToomW) >> 7) + 1);
+}
+constexpr int kToomStgStride = toom_stg_stride(kToomBlk);
 
 struct ToomIn {
     const uint32_t *C;  // item base (5 products)
@@ -492,30 +495,31 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
 // XORed after a barrier): no c_j round trip through HBM, one launch.
+template <int BLK>
 __global__ void __launch_bounds__(kToomScanT, 3)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS) {
     extern __shared__ uint32_t tsm[];
-    constexpr int W = kToomW, ROWS = kToomBlk / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
-    constexpr int H = kToomBlk + 3 * W;
-    constexpr int HP = kToomStgStride;  // padded stride per input (see tstg)
+    constexpr int W = kToomW, ROWS = BLK / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
+    constexpr int H = BLK + 3 * W;
+    constexpr int HP = toom_stg_stride(BLK);  // padded stride per input (see tstg)
     uint32_t *Stg = tsm;  // [5][HP]
     __shared__ uint32_t stot[3][NSEG][W];
     __shared__ uint32_t bcar[3][W];  // carry into the current block, per chain
     const int64_t item = blockIdx.x;
-    const int L = 2 * M, nb = (L + kToomBlk - 1) / kToomBlk;
+    const int L = 2 * M, nb = (L + BLK - 1) / BLK;
     const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
     uint32_t *Rg = R + item * outS;
     const bool plain = LFi == LFSi;
     // quad staging: plain inputs whose item/row offsets and length are whole
-    // quads (block starts are multiples of 4: kToomBlk and 2w are)
+    // quads (block starts are multiples of 4: BLK and 2w are)
     const bool vec = plain && (inS % 4) == 0 && (Lin % 4) == 0 &&
                      (reinterpret_cast<uintptr_t>(Cin) & 15) == 0;
     const int r = int(threadIdx.x) % W, sg = int(threadIdx.x) / W;
     if (threadIdx.x < 3 * W) bcar[threadIdx.x / W][threadIdx.x % W] = 0u;
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
-        const int k0 = b * kToomBlk, kb = k0 - 2 * W;
+        const int k0 = b * BLK, kb = k0 - 2 * W;
         if (vec) {  // plain, 16-byte aligned inputs: quads, all in flight per half
             constexpr int T = kToomScanT, H4 = H / 4, NQ = (5 * H4 + T - 1) / T, NH = (NQ + 1) / 2;
             __syncthreads();  // previous block's readers of Stg / stot are done
@@ -627,19 +631,20 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         __syncthreads();
         // ... second contributions XOR onto them (written by this CTA, earlier
         // or before the barrier above); loads of a half batch first
+        constexpr int HB = (SEGR + 1) / 2;  // rows per half batch (SEGR may be odd)
 #pragma unroll
-        for (int h2 = 0; h2 < SEGR; h2 += SEGR / 2) {
-            uint32_t old[SEGR / 2][4];
+        for (int h2 = 0; h2 < SEGR; h2 += HB) {
+            uint32_t old[HB][4];
 #pragma unroll
-            for (int i = 0; i < SEGR / 2; ++i) {
+            for (int i = 0; i < HB; ++i) {
                 const int k = kr + (h2 + i) * W;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) old[i][j] = (k < L && k >= M) ? Rg[k + j * M] : 0u;
+                for (int j = 0; j < 4; ++j) old[i][j] = (h2 + i < SEGR && k < L && k >= M) ? Rg[k + j * M] : 0u;
             }
 #pragma unroll
-            for (int i = 0; i < SEGR / 2; ++i) {
+            for (int i = 0; i < HB; ++i) {
                 const int k = kr + (h2 + i) * W;
-                if (k < L && k >= M) {
+                if (h2 + i < SEGR && k < L && k >= M) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ keep[h2 + i][j];
                 }
@@ -923,6 +928,16 @@ static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
 // Toom interpolation: levels with >= this many products use the one-CTA-per-
 // product kernel (F2X_TOOM_SEQ overrides; measured: 512 products sequential
 // (n=57637 level 1: 263 vs 389 us), 128 two-kernel (n=35851 level 1))
+// F2X_TOOM_BLK=2048 pins the sequential interpolation to 2048-coefficient
+// blocks (experiments)
+static int toom_blk_choice() {
+    static const int v = [] {
+        const char *e = getenv("F2X_TOOM_BLK");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 static int64_t toom_seq_min() {
     static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
@@ -1332,13 +1347,25 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sms));
             if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sms));
+                ae = cudaFuncSetAttribute(toom_interp_seq<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(5 * toom_stg_stride(2048) * 4));
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_interp_seq<2304>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(5 * toom_stg_stride(2304) * 4));
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             attr_dev_mask.fetch_or(1u << dev);
         }
         if (seq) {
-            toom_interp_seq<<<unsigned(items), kToomScanT, sms, stream>>>(root, out, M, rootLF, rootLFS, rootS,
-                                                                          Lin, outS);
+            // block size per level: the CTA walks its 2M coefficients in blocks
+            // whose cost is mostly fixed latency, so take 2304 when it saves
+            // a block (n=57637 level 3: 2M = 4300 -> 2 blocks instead of 3)
+            if (ceil_div(2 * M, 2304) < ceil_div(2 * M, 2048) && toom_blk_choice() != 2048) {
+                toom_interp_seq<2304><<<unsigned(items), kToomScanT, 5 * toom_stg_stride(2304) * 4, stream>>>(
+                    root, out, M, rootLF, rootLFS, rootS, Lin, outS);
+            } else {
+                toom_interp_seq<2048><<<unsigned(items), kToomScanT, 5 * toom_stg_stride(2048) * 4, stream>>>(
+                    root, out, M, rootLF, rootLFS, rootS, Lin, outS);
+            }
             if ((rc = debug_sync(stream, 5))) return rc;
         } else {
             toom_interp_scan<<<unsigned(items * nb), kToomScanT, sms, stream>>>(root, Q, Tot, M, kToomW, rootLF,
