@@ -96,7 +96,9 @@ def committed_traffic(pl) -> dict | None:
             el = pl.get("eval_levels", 0)
             ns = 3 ** el * (pl["leaf_stride"] << (pl["levels"] - el))
             ss = pl["leaf_stride"] << pl["cta_levels"]
-            alg = 4 * pl["groups"] * (2 * ns + 3 ** pl["global_levels"] * 2 * ss)
+            # (with cluster combining the node kernel writes the 3^(GL-1) parents, 4 Ss words each)
+            cl = pl.get("cluster_levels", 0)
+            alg = 4 * pl["groups"] * (2 * ns + 3 ** (pl["global_levels"] - cl) * 2 * (ss << cl))
             best = {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"],
                     "algorithmic_bytes_per_launch": alg,
                     "note": "DRAM < algorithmic: L2 (126 MB) absorbs most node-product writes"}
@@ -407,7 +409,7 @@ def gpu_arm(args) -> None:
                 "parallelism": f"independent batch shards x{world}, no collectives",
                 "l2": "flushed before each timed step (256 MiB write, outside events)",
                 "plan": {k: pl[k] for k in ("N", "leaf_words", "levels", "cta_levels",
-                                             "global_levels", "pass_levels", "node_ctas")},
+                                             "global_levels", "pass_levels", "cluster_levels", "node_ctas")},
             },
             "roofline": {
                 "bound": "int_alu",

@@ -938,6 +938,18 @@ static int toom_blk_choice() {
     return v;
 }
 
+// F2X_CLUSTER=1: combine the deepest global level inside 3-CTA clusters of
+// the node kernel (distributed shared memory).  Off by default: measured
+// 15-18 % slower node kernel (cluster gang scheduling and the two cluster
+// barriers idle CTA slots) for a saved interpolation level.
+static bool cluster_combine_enabled() {
+    static const bool v = [] {  // thread-safe one-time read
+        const char *e = getenv("F2X_CLUSTER");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 static int64_t toom_seq_min() {
     static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
@@ -1018,7 +1030,10 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->levels = K;
     pl->cta_levels = KC;
     pl->global_levels = GL;
-    int rem = GL, np = 0;
+    // optionally the deepest global level is combined inside 3-CTA clusters
+    // of the node kernel (F2X_CLUSTER=1; off by default, see above)
+    const int CL = (GL >= 1 && cluster_combine_enabled()) ? 1 : 0;
+    int rem = GL - CL, np = 0;
     while (rem > 0) {
         const int p = std::min(kMaxPassLevels, rem);
         pl->pass_levels[np++] = p;
@@ -1029,6 +1044,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
+    pl->cluster_levels = CL;
     pl->toom_levels = TL;
     pl->toom_w = TL ? kToomW : 0;
     for (int l = 1; l <= TL; ++l) pl->toom_M[l - 1] = int32_t(bestM[l]);
@@ -1065,11 +1081,11 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.off_abs = off;
     L.off_bbs = align256(L.off_abs + opw * 4);
     L.off_p0 = align256(L.off_bbs + opw * 4);
-    const int64_t p0 = G2 * ipow3(GL) * 2 * L.Ss * 4;
+    const int64_t p0 = G2 * ipow3(GL - CL) * 2 * (L.Ss << CL) * 4;  // node (or cluster parent) products
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
     if (np >= 1) {  // first pass output (the largest one written to P1)
-        const int d1 = GL - pl->pass_levels[0];
+        const int d1 = GL - CL - pl->pass_levels[0];
         p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
     off = align256(L.off_p1 + p1);
@@ -1086,7 +1102,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     }
     L.total = off;
     {  // every pass output must fit the ping-pong buffer it is written to
-        int d = GL;
+        int d = GL - CL;
         for (int i = 0; i < np; ++i) {
             const int dlo = d - pl->pass_levels[i];
             const int64_t outb = G2 * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
@@ -1262,6 +1278,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.GL = pl.global_levels - L.el;
     kp.paths = int(ipow3(pl.global_levels - L.el));
     kp.prof = nullptr;
+    kp.combine = pl.cluster_levels;
     const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
     if (prof_path) {
         cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
@@ -1297,7 +1314,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     }
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
-    int d = pl.global_levels;
+    int d = pl.global_levels - pl.cluster_levels;
     for (int i = 0; i < pl.num_passes; ++i) {
         const int D = pl.pass_levels[i];
         const int dlo = d - D;
