@@ -80,12 +80,14 @@ typedef struct f2x_plan {
                                 (node kernel runs on 5^toom_levels x groups) */
     int32_t toom_w;          /* Toom-3 point x = X^toom_w                      */
     int32_t toom_M[4];       /* part size (coefficients) of Toom level 1..     */
-    int32_t cluster_levels;  /* 1: the deepest global Karatsuba level is
-                                combined by the node kernel itself -- the 3
-                                sibling node CTAs form a thread-block cluster
-                                and build their parent product through
-                                distributed shared memory; 0: every level is
-                                an interpolation pass                        */
+    int32_t fused_levels;    /* 1: the deepest global Karatsuba level is
+                                combined inside the node kernel (fuse_mode),
+                                the interpolation passes start one level up */
+    int32_t fuse_mode;       /* 0 none; 1: the 3 sibling node CTAs form a
+                                thread-block cluster and build the parent
+                                through distributed shared memory; 2: the last
+                                sibling to finish (atomic counter) builds the
+                                parent in place from the L2-resident products */
 } f2x_plan;
 
 /* Fill *plan for a call shape.  leaf_hint = 0 picks the default leaf;

@@ -865,6 +865,7 @@ struct Layout {
     int64_t off_r[kMaxToom + 1] = {};  // Toom interpolation outputs, level l
     int64_t off_q[kMaxToom + 1] = {};  // level-l c_0..c_4 before carries (5 x 2M per item)
     int64_t off_tot[kMaxToom + 1] = {};  // level-l chain totals per block
+    int64_t off_cnt = 0;             // fuse mode 2: per-parent arrival counters
 };
 
 // Top global levels pre-evaluated by the slicing kernel (k1_slice_eval):
@@ -938,14 +939,17 @@ static int toom_blk_choice() {
     return v;
 }
 
-// F2X_CLUSTER=1: combine the deepest global level inside 3-CTA clusters of
-// the node kernel (distributed shared memory).  Off by default: measured
-// 15-18 % slower node kernel (cluster gang scheduling and the two cluster
-// barriers idle CTA slots) for a saved interpolation level.
-static bool cluster_combine_enabled() {
-    static const bool v = [] {  // thread-safe one-time read
-        const char *e = getenv("F2X_CLUSTER");
-        return e && e[0] == '1';
+// Combining the deepest global Karatsuba level inside the node kernel
+// (F2X_FUSE, read once): 0 off (default: a separate interpolation pass);
+// 1 3-CTA clusters + distributed shared memory (node kernel 15-18 % slower:
+// cluster gang scheduling and two cluster barriers idle CTA slots); 2 the
+// last-arriving sibling builds the parent in place (node kernel ~8 % slower:
+// the finishing CTA's memory work holds an ALU-bound CTA slot).  Both cost
+// more than the pass they save.
+static int fuse_mode_env() {
+    static const int v = [] {
+        const char *e = getenv("F2X_FUSE");
+        return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
     }();
     return v;
 }
@@ -1030,9 +1034,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->levels = K;
     pl->cta_levels = KC;
     pl->global_levels = GL;
-    // optionally the deepest global level is combined inside 3-CTA clusters
-    // of the node kernel (F2X_CLUSTER=1; off by default, see above)
-    const int CL = (GL >= 1 && cluster_combine_enabled()) ? 1 : 0;
+    // the deepest global level combined inside the node kernel (fuse_mode_env)
+    const int FM = GL >= 1 ? fuse_mode_env() : 0;
+    const int CL = FM ? 1 : 0;
     int rem = GL - CL, np = 0;
     while (rem > 0) {
         const int p = std::min(kMaxPassLevels, rem);
@@ -1044,7 +1048,8 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
-    pl->cluster_levels = CL;
+    pl->fused_levels = CL;
+    pl->fuse_mode = FM;
     pl->toom_levels = TL;
     pl->toom_w = TL ? kToomW : 0;
     for (int l = 1; l <= TL; ++l) pl->toom_M[l - 1] = int32_t(bestM[l]);
@@ -1081,7 +1086,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.off_abs = off;
     L.off_bbs = align256(L.off_abs + opw * 4);
     L.off_p0 = align256(L.off_bbs + opw * 4);
-    const int64_t p0 = G2 * ipow3(GL - CL) * 2 * (L.Ss << CL) * 4;  // node (or cluster parent) products
+    // node products (mode 2: parents overwrite their triple's first 4 Ss words), or
+    // the cluster parents (mode 1)
+    const int64_t p0 = FM == 1 ? G2 * ipow3(GL - 1) * 4 * L.Ss * 4 : G2 * ipow3(GL) * 2 * L.Ss * 4;
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
     if (np >= 1) {  // first pass output (the largest one written to P1)
@@ -1089,6 +1096,8 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
     off = align256(L.off_p1 + p1);
+    L.off_cnt = off;  // mode-2 arrival counters, one per parent
+    if (FM == 2) off = align256(off + G2 * ipow3(GL - 1) * 4);
     for (int l = TL; l >= 1; --l) {  // Toom interpolation: [block scans, totals,] outputs
         const int64_t items = G * ipow5(l - 1);
         L.off_q[l] = L.off_tot[l] = off;
@@ -1278,7 +1287,13 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.GL = pl.global_levels - L.el;
     kp.paths = int(ipow3(pl.global_levels - L.el));
     kp.prof = nullptr;
-    kp.combine = pl.cluster_levels;
+    kp.combine = pl.fuse_mode;
+    kp.cnt = nullptr;
+    if (pl.fuse_mode == 2) {
+        kp.cnt = reinterpret_cast<unsigned *>(w + L.off_cnt);
+        const cudaError_t me = cudaMemsetAsync(kp.cnt, 0, size_t(pl.node_ctas / 3) * 4, stream);
+        if (me != cudaSuccess) return F2X_ECUDA - int(me);
+    }
     const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
     if (prof_path) {
         cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
@@ -1314,18 +1329,22 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     }
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
-    int d = pl.global_levels - pl.cluster_levels;
+    int d = pl.global_levels - pl.fused_levels;
+    // stride of the first pass's input products (mode 2: parents in place of
+    // their triple, 6 Ss words apart)
+    int64_t in_stride0 = pl.fuse_mode == 2 ? 6 * L.Ss : 2 * (L.Ns >> d);
     for (int i = 0; i < pl.num_passes; ++i) {
         const int D = pl.pass_levels[i];
         const int dlo = d - D;
         const int64_t Shi = L.Ns >> d, Slo = L.Ns >> dlo;
         const int qw = int(Shi / 2);
         const int64_t items = L.G2 * ipow3(dlo) * qw;
+        const int64_t inS = i == 0 ? in_stride0 : 2 * Shi;
         switch (D) {
-            case 1: launch_k3<1>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
-            case 2: launch_k3<2>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
-            case 3: launch_k3<3>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
-            case 4: launch_k3<4>(cur, nxt, items, qw, 2 * Shi, 2 * Slo, stream); break;
+            case 1: launch_k3<1>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 2: launch_k3<2>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 3: launch_k3<3>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 4: launch_k3<4>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
             default: return F2X_ERANGE;
         }
         if (getenv("F2X_DEBUG_SYNC"))
@@ -1344,7 +1363,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // products of the level below
     const uint32_t *root = cur;
     int rootLF = pl.leaf_words, rootLFS = pl.leaf_stride;
-    int64_t rootS = 2 * L.Ns;
+    int64_t rootS = pl.num_passes == 0 ? in_stride0 : 2 * L.Ns;
     for (int l = L.tl; l >= 1; --l) {
         uint32_t *out = reinterpret_cast<uint32_t *>(w + L.off_r[l]);
         uint32_t *Q = reinterpret_cast<uint32_t *>(w + L.off_q[l]);
