@@ -492,6 +492,8 @@ def extra_configs(torch, np, dev, args, peak) -> dict:
             e1.record()
             torch.cuda.synchronize()
             tot += e0.elapsed_time(e1)
+            if os.environ.get("F2X_BENCH_DEBUG"):
+                print(f"extra n={n} rep {i}: {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
         ms = tot / reps
         t = (n + 63) // 64
         v = batch / (ms / 1e3)
