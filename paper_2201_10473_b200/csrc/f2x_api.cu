@@ -52,6 +52,15 @@ static constexpr double kToomWordCost = 15.0;  // planner: cost units per word m
 static constexpr int kToomMinWords = 544;      // Toom only above 512 words: d=32768 (t=512) measured 4.6 % slower with it
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// every pipeline kernel goes through launch_pdl (programmatic dependent launch)
+#define F2X_LAUNCH(kern, grid, block, smem, stream, ...)                                          \
+    do {                                                                                          \
+        const cudaError_t le_ = launch_pdl(kern, dim3(grid), dim3(block), size_t(smem), stream,   \
+                                           __VA_ARGS__);                                          \
+        if (le_ != cudaSuccess) return F2X_ECUDA - int(le_);                                      \
+    } while (0)
+
 static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 static inline int64_t ipow5(int k) {
     int64_t r = 1;
@@ -115,6 +124,7 @@ __global__ void __launch_bounds__(kTileThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
          uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
          int ncyc, uint32_t *d_err, int tiles) {
+    pdl_prologue();
     __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
@@ -173,6 +183,7 @@ __global__ void __launch_bounds__(kTileThreads << EL)
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
               int ncyc, uint32_t *d_err, int tiles, int TW) {
+    pdl_prologue();
     // TW (<= 64) operand words per tile: the part is cut into `tiles`
     // balanced tiles, so no CTA carries a nearly empty tail tile
     constexpr int NP = 1 << EL;               // parts
@@ -254,6 +265,7 @@ __global__ void __launch_bounds__(256)
 toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
                 uint32_t *__restrict__ Yb, int64_t items_in, int64_t inS, int M, int w, int S, int LFo,
                 int LFSo, int64_t outS) {
+    pdl_prologue();
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= items_in * outS) return;
     const int64_t i = idx / outS;
@@ -296,6 +308,7 @@ toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb
 __global__ void __launch_bounds__(256)
 toom_eval_level_q(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
                   uint32_t *__restrict__ Yb, int64_t inS, int M, int w, int S, int LFo, int LFSo, int64_t outS) {
+    pdl_prologue();
     const int sq = int(blockIdx.x) * 256 + int(threadIdx.x);
     const int sw0 = 4 * sq;
     if (sw0 >= outS) return;
@@ -388,6 +401,7 @@ struct ToomIn {
 __global__ void __launch_bounds__(kToomScanT)
 toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uint32_t *__restrict__ Tot, int M,
                  int w, int LFi, int LFSi, int64_t inS, int Lin, int nb) {
+    pdl_prologue();
     extern __shared__ uint32_t tsm[];
     const int H = kToomBlk + 3 * w;          // staged span per input
     constexpr int HP = kToomStgStride;        // padded stride per input (see tstg)
@@ -499,6 +513,7 @@ template <int BLK>
 __global__ void __launch_bounds__(kToomScanT, 3)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS) {
+    pdl_prologue();
     extern __shared__ uint32_t tsm[];
     constexpr int W = kToomW, ROWS = BLK / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
     constexpr int H = BLK + 3 * W;
@@ -664,6 +679,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
 __global__ void __launch_bounds__(256)
 toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict__ Tot, uint32_t *__restrict__ R,
                      int M, int w, int nb, int nbo, int64_t outS) {
+    pdl_prologue();
     extern __shared__ uint32_t carry[];  // [nb][3][w]
     const int64_t item = blockIdx.x / nbo;
     const int ob = int(blockIdx.x - item * nbo);
@@ -773,6 +789,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t items, int qw,
           int64_t inStride, int64_t outStride) {
+    pdl_prologue();
     // blocks walk the nodes in REVERSE order: the node kernel wrote them in
     // forward order, so the most recently written (still L2-resident)
     // products are consumed first instead of being evicted by the rest
@@ -797,6 +814,7 @@ template <int TW>
 __global__ void __launch_bounds__(2 * TW)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
+    pdl_prologue();
     constexpr int TC = 64 * TW, TT = 2 * TW;  // coefficients, threads per tile
     __shared__ uint32_t stage[TC + TC / 32];
     const int tid = threadIdx.x;
@@ -1128,9 +1146,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
 template <int D>
 static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw, int64_t inS,
                      int64_t outS, cudaStream_t s) {
-    k3_interp<D><<<unsigned(ceil_div(items, kThreads)), kThreads, 0, s>>>(Pin, Pout, items, qw,
-                                                                            inS, outS);
-    return 0;
+    const cudaError_t e = launch_pdl(k3_interp<D>, dim3(unsigned(ceil_div(items, kThreads))), dim3(kThreads), 0, s,
+                                     Pin, Pout, items, qw, inS, outS);
+    return e == cudaSuccess ? 0 : F2X_ECUDA - int(e);
 }
 
 // Optional per-thread events recorded around the node kernel (bench.py uses
@@ -1203,7 +1221,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
         uint32_t *X0a = reinterpret_cast<uint32_t *>(w + L.off_x[0]);
-        k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, X0a, X0a + G * int64_t(pl.N), batch, pl.t, pl.N,
+        F2X_LAUNCH(k1_slice, grid, kTileThreads, 0, stream, A, B, X0a, X0a + G * int64_t(pl.N), batch, pl.t, pl.N,
                                                     pl.N, pl.N, int64_t(pl.N), ncyc, d_err, tiles);
         if ((rc = debug_sync(stream, 1))) return rc;
         // Toom evaluation levels: level l < tl writes plain operands of
@@ -1232,11 +1250,11 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             }
             if (outS % 4 == 0 && (LFo == LFSo || LFSo % 4 == 0) && items_in <= 65535) {
                 dim3 grid(unsigned(ceil_div(outS / 4, 256)), unsigned(items_in), 2);
-                toom_eval_level_q<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, inS, int(L.M[l]), kToomW, S, LFo,
+                F2X_LAUNCH(toom_eval_level_q, grid, 256, 0, stream, xa, xb, ya, yb, inS, int(L.M[l]), kToomW, S, LFo,
                                                             LFSo, outS);
             } else {
                 dim3 grid(unsigned(ceil_div(items_in * outS, 256)), 2);
-                toom_eval_level<<<grid, 256, 0, stream>>>(xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
+                F2X_LAUNCH(toom_eval_level, grid, 256, 0, stream, xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
                                                           S, LFo, LFSo, outS);
             }
             if ((rc = debug_sync(stream, 1))) return rc;
@@ -1244,7 +1262,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     } else if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
-        k1_slice<<<grid, kTileThreads, 0, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+        F2X_LAUNCH(k1_slice, grid, kTileThreads, 0, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                     pl.leaf_words, pl.leaf_stride, L.Ns, ncyc,
                                                     d_err, tiles);
     } else {
@@ -1266,11 +1284,11 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             attr_dev_mask[L.el].fetch_or(1u << dev);
         }
         if (L.el == 1) {
-            k1_slice_eval<1><<<grid, kTileThreads << 1, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+            F2X_LAUNCH(k1_slice_eval<1>, grid, kTileThreads << 1, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
                                                                  L.Ns >> 1, ncyc, d_err, tiles, TW);
         } else {
-            k1_slice_eval<2><<<grid, kTileThreads << 2, sm, stream>>>(A, B, Abs, Bbs, batch, pl.t, pl.N,
+            F2X_LAUNCH(k1_slice_eval<2>, grid, kTileThreads << 2, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
                                                                  L.Ns >> 2, ncyc, d_err, tiles, TW);
         }
@@ -1341,12 +1359,13 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int64_t items = L.G2 * ipow3(dlo) * qw;
         const int64_t inS = i == 0 ? in_stride0 : 2 * Shi;
         switch (D) {
-            case 1: launch_k3<1>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 2: launch_k3<2>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 3: launch_k3<3>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 4: launch_k3<4>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 1: rc = launch_k3<1>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 2: rc = launch_k3<2>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 3: rc = launch_k3<3>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 4: rc = launch_k3<4>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
             default: return F2X_ERANGE;
         }
+        if (rc) return rc;
         if (getenv("F2X_DEBUG_SYNC"))
             fprintf(stderr, "f2x pass %d: D=%d d=%d dlo=%d qw=%d items=%lld inS=%lld outS=%lld "
                     "cur=%s maxread=%lld maxwrite=%lld p0=%lld p1=%lld\n", i, D, d, dlo, qw,
@@ -1396,19 +1415,19 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             // whose cost is mostly fixed latency, so take 2304 when it saves
             // a block (n=57637 level 3: 2M = 4300 -> 2 blocks instead of 3)
             if (ceil_div(2 * M, 2304) < ceil_div(2 * M, 2048) && toom_blk_choice() != 2048) {
-                toom_interp_seq<2304><<<unsigned(items), kToomScanT, 5 * toom_stg_stride(2304) * 4, stream>>>(
+                F2X_LAUNCH(toom_interp_seq<2304>, unsigned(items), kToomScanT, 5 * toom_stg_stride(2304) * 4, stream, 
                     root, out, M, rootLF, rootLFS, rootS, Lin, outS);
             } else {
-                toom_interp_seq<2048><<<unsigned(items), kToomScanT, 5 * toom_stg_stride(2048) * 4, stream>>>(
+                F2X_LAUNCH(toom_interp_seq<2048>, unsigned(items), kToomScanT, 5 * toom_stg_stride(2048) * 4, stream, 
                     root, out, M, rootLF, rootLFS, rootS, Lin, outS);
             }
             if ((rc = debug_sync(stream, 5))) return rc;
         } else {
-            toom_interp_scan<<<unsigned(items * nb), kToomScanT, sms, stream>>>(root, Q, Tot, M, kToomW, rootLF,
+            F2X_LAUNCH(toom_interp_scan, unsigned(items * nb), kToomScanT, sms, stream, root, Q, Tot, M, kToomW, rootLF,
                                                                                 rootLFS, rootS, Lin, nb);
             if ((rc = debug_sync(stream, 5))) return rc;
             const size_t sm = size_t(nb) * 3 * kToomW * 4;
-            toom_interp_assemble<<<unsigned(items * nbo), 256, sm, stream>>>(Q, Tot, out, M, kToomW, nb, nbo,
+            F2X_LAUNCH(toom_interp_assemble, unsigned(items * nbo), 256, sm, stream, Q, Tot, out, M, kToomW, nb, nbo,
                                                                              outS);
             if ((rc = debug_sync(stream, 5))) return rc;
         }
@@ -1423,7 +1442,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         // under one wave at 64 words)
         constexpr int TW4 = 32;
         const int tiles = int(ceil_div(tout, TW4));
-        k4_unslice<TW4><<<unsigned(G * tiles), 2 * TW4, 0, stream>>>(
+        F2X_LAUNCH(k4_unslice<TW4>, unsigned(G * tiles), 2 * TW4, 0, stream, 
             root, C, batch, tout, rootLF, rootLFS, rootS, ncyc, tiles);
     }
     if ((rc = debug_sync(stream, 4))) return rc;

@@ -28,6 +28,46 @@ namespace f2x {
 
 __host__ __device__ constexpr int pow3c(int k) { return k <= 0 ? 1 : 3 * pow3c(k - 1); }
 
+// Programmatic dependent launch (F2X_PDL=1: every kernel of a call is launched
+// with programmatic stream serialisation, see launch_pdl): a kernel lets its
+// successor's CTAs launch once all of its own CTAs are running, and waits for
+// its predecessor's completion (and memory) before touching anything, so
+// launch latency and wave tails overlap across the call's kernels.  Both
+// instructions are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+// F2X_PDL=1 launches with the programmatic serialisation attribute.  Off by
+// default: measured 1-2 % slower per call (n=17669 0.3375 -> 0.3412 ms,
+// n=35851 0.964 -> 0.972 ms) -- the successor's early-resident CTAs only
+// wait, while holding registers and shared memory during the predecessor's
+// tail.
+inline bool pdl_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("F2X_PDL");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // chunk stride in words for leaf size LF (see the layout note above)
 __host__ __device__ constexpr int leaf_stride_words(int LF) {
     return 4 * ((((LF + 3) / 4) % 2) ? (LF + 3) / 4 : (LF + 3) / 4 + 1);
@@ -874,6 +914,7 @@ k2_node_mul(const K2Params p, int64_t nodes) {
     __shared__ uint16_t pos[C::NPOS];  // node positions (quads), level-major
     __shared__ uint8_t mtab[KC == 5 ? 2 * 81 : 1];  // mid-leaf permutation + inverse (KC = 5)
 
+    pdl_prologue();
     const int tid = threadIdx.x;
     const int64_t node = blockIdx.x;
     (void)nodes;
@@ -998,8 +1039,9 @@ int launch_k2(const K2Params &p, int64_t blocks, cudaStream_t stream) {
         e = cudaLaunchKernelEx(&cfg, k2_node_mul<LF, KC>, p, blocks);
         if (e == cudaSuccess) e = cudaGetLastError();
     } else {
-        k2_node_mul<LF, KC><<<dim3(unsigned(blocks)), C::NT, C::SMEM + pad, stream>>>(p, blocks);
-        e = cudaGetLastError();
+        e = launch_pdl(k2_node_mul<LF, KC>, dim3(unsigned(blocks)), dim3(C::NT), C::SMEM + pad, stream, p,
+                       blocks);
+        if (e == cudaSuccess) e = cudaGetLastError();
     }
     return e == cudaSuccess ? 0 : -1000 - int(e);
 }
