@@ -243,7 +243,77 @@ __device__ __forceinline__ void node_load_direct(const K2Params &p, int64_t g, u
     }
 }
 
-// One Karatsuba level.  ITER = ceil(items/NTH) is a compile-time constant and
+// Operand load fused with the first evaluation pair (levels 0 and 1; KC >= 3):
+// item (operand, w) gathers the root operand's four quarter quads at w from
+// the path's segments, stores them, and writes the level-0 mid (2 quads) and
+// the three level-1 mids (3 quads) straight from registers -- one barrier and
+// the pair's shared-memory reads fewer than load + eval_pair<0>.
+template <int LF, int KC, int NTH>
+__device__ __forceinline__ void node_load_eval0(const K2Params &p, int64_t g, uint32_t base, uint32_t mids,
+                                                uint4 *As, uint4 *Bs, int t) {
+    using C = K2Cfg<LF, KC>;
+    constexpr int q = C::Q << (KC - 2);                 // root quarter, quads
+    constexpr int SQ = C::SQ;                           // = 4 q
+    constexpr int Rj1 = C::Q * (1 << (KC - 1)) * 3;     // level-1 mids (eval_pair<0>)
+    constexpr int ITEMS = (2 * q + NTH - 1) / NTH;
+    uint4 x[ITEMS][4];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[i][k] = make_uint4(0, 0, 0, 0);
+    const bool two = mids != 0;
+    uint32_t sub = 0;
+#pragma unroll 1
+    do {
+        const uint32_t o0 = (base + sub) * C::Q;
+        sub = (sub - mids) & mids;
+        const uint32_t o1 = (base + sub) * C::Q;
+        if (two) sub = (sub - mids) & mids;
+        uint4 y[ITEMS][4][2];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int it = t + i * NTH;
+            if ((2 * q) % NTH == 0 || it < 2 * q) {
+                const int op = it >= q, w = it - op * q;
+                const uint4 *G = reinterpret_cast<const uint4 *>(op ? p.Bbs : p.Abs) + g * (p.Ns / 4) + w;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    y[i][k][0] = __ldg(G + o0 + k * q);
+                    if (two) y[i][k][1] = __ldg(G + o1 + k * q);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int it = t + i * NTH;
+            if ((2 * q) % NTH == 0 || it < 2 * q) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    x[i][k] = x[i][k] ^ y[i][k][0];
+                    if (two) x[i][k] = x[i][k] ^ y[i][k][1];
+                }
+            }
+        }
+    } while (sub != 0);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int it = t + i * NTH;
+        if ((2 * q) % NTH == 0 || it < 2 * q) {
+            const int op = it >= q, w = it - op * q;
+            uint4 *X = op ? Bs : As;
+            const uint4 m0 = x[i][0] ^ x[i][2], m1 = x[i][1] ^ x[i][3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) X[w + k * q] = x[i][k];
+            X[SQ + w] = m0;
+            X[SQ + q + w] = m1;
+            X[Rj1 + w] = x[i][0] ^ x[i][1];
+            X[Rj1 + q + w] = x[i][2] ^ x[i][3];
+            X[Rj1 + 2 * q + w] = m0 ^ m1;
+        }
+    }
+}
+
+// One Karatsuba level.  ITER = ceil(items/NTH) is a compile-time constant and// One Karatsuba level.  ITER = ceil(items/NTH) is a compile-time constant and
 // items are processed in unrolled batches of UNR: all shared-memory loads of
 // a batch are issued before its first XOR (one smem round trip per batch
 // instead of one per item) while the register footprint stays bounded.
@@ -424,6 +494,10 @@ __device__ __forceinline__ void interp_pair(uint4 *As, uint4 *Bs, const uint16_t
 // chunk (single leaf code path, no barriers inside the leaf phase).
 #ifndef F2X_PROF_BUILD
 #define F2X_PROF_BUILD 0
+#endif
+
+#ifndef F2X_FUSED_LOAD_EVAL
+#define F2X_FUSED_LOAD_EVAL 1
 #endif
 
 #ifndef F2X_FUSED_STORE
@@ -951,7 +1025,9 @@ k2_node_mul(const K2Params p, int64_t nodes) {
     uint32_t base, mids;
     path_base_mids(p, path, base, mids);
     mark(0);
-    node_load_direct<LF, KC, C::NT>(p, g, base, mids, As, Bs, tid);
+    constexpr bool kFuseEval0 = F2X_FUSED_LOAD_EVAL && kEvalLevels(KC) >= 2;
+    if constexpr (kFuseEval0) node_load_eval0<LF, KC, C::NT>(p, g, base, mids, As, Bs, tid);
+    else node_load_direct<LF, KC, C::NT>(p, g, base, mids, As, Bs, tid);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int e = tid + i * C::NT;
@@ -960,7 +1036,8 @@ k2_node_mul(const K2Params p, int64_t nodes) {
     if (KC == 5 && tid < 2 * 81) mtab[tid] = uint8_t(mt);
     __syncthreads();
     mark(1);
-    node_eval<LF, KC, C::NT>(As, Bs, pos, tid, SyncAll{});
+    if constexpr (kFuseEval0) node_eval_from<LF, KC, C::NT, 2>(As, Bs, pos, tid, SyncAll{});
+    else node_eval<LF, KC, C::NT>(As, Bs, pos, tid, SyncAll{});
     mark(2);
     node_leaves<LF, KC>(As, Bs, pos, mtab, tid, SyncAll{});
     __syncthreads();
