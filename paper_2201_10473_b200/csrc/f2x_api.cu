@@ -1411,10 +1411,13 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             attr_dev_mask.fetch_or(1u << dev);
         }
         if (seq) {
-            // block size per level: the CTA walks its 2M coefficients in blocks
-            // whose cost is mostly fixed latency, so take 2304 when it saves
-            // a block (n=57637 level 3: 2M = 4300 -> 2 blocks instead of 3)
-            if (ceil_div(2 * M, 2304) < ceil_div(2 * M, 2048) && toom_blk_choice() != 2048) {
+            // block size per level: 2304-coefficient blocks (9 rows per scan
+            // segment) cost ~10 % more per coefficient than 2048 (8 rows), so
+            // they are taken only when they stage clearly fewer coefficients:
+            // n=57637 level 3 (2M = 4300: 2 blocks instead of 3, 704 -> 592
+            // us); levels 1-2 measured 4-10 % slower with 2304
+            const int64_t nb2048 = ceil_div(2 * M, 2048), nb2304 = ceil_div(2 * M, 2304);
+            if (double(nb2304) * 2304 * 1.1 < double(nb2048) * 2048 && toom_blk_choice() != 2048) {
                 F2X_LAUNCH(toom_interp_seq<2304>, unsigned(items), kToomScanT, 5 * toom_stg_stride(2304) * 4, stream, 
                     root, out, M, rootLF, rootLFS, rootS, Lin, outS);
             } else {
