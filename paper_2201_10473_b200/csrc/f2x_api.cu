@@ -560,22 +560,41 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         } else         {  // staging: every load of the block in flight at once
             constexpr int T = kToomScanT, NI = (H + T - 1) / T;
             uint32_t v[5][NI];
-#pragma unroll
-            for (int e = 0; e < 5; ++e) {
+            // storage offset of coefficient k = kb + tid + i T, walked
+            // incrementally (one chunk split per block instead of one per
+            // word; the per-word split was the kernel's top cost)
+            int off[NI];
+            bool ok[NI];
+            {
+                const int k0w = kb + int(threadIdx.x);
+                const int kk = k0w < 0 ? 0 : k0w;  // (negative k only in block 0, masked below)
+                int c = plain ? 0 : kk / LFi, rr = plain ? kk : kk - c * LFi;
+                const int dc = plain ? 0 : T / LFi, dr = plain ? T : T - dc * LFi;
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
                     const int h = int(threadIdx.x) + i * T, k = kb + h;
-                    uint32_t x = 0;
-                    if (h < H && k >= 0 && k < Lin) {
-                        int64_t off = k;
-                        if (!plain) {
-                            const int c = __float2int_rz((float(k) + 0.5f) * in.invLF);
-                            off = int64_t(c) * LFSi + (k - c * LFi);
+                    ok[i] = h < H && k >= 0 && k < Lin;
+                    off[i] = plain ? k : c * LFSi + rr;
+                    if (k0w < 0 && k + T >= 0 && k < 0) {  // the walk starts at the first k >= 0
+                        const int kn = k + T;
+                        c = plain ? 0 : kn / LFi;
+                        rr = plain ? kn : kn - c * LFi;
+                    } else if (k >= 0) {
+                        rr += dr;
+                        c += dc;
+                        if (!plain && rr >= LFi) {
+                            rr -= LFi;
+                            ++c;
                         }
-                        x = __ldg(in.C + e * inS + off);
                     }
-                    v[e][i] = x;
                 }
+            }
+            const uint32_t *Ce = in.C;
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+#pragma unroll
+                for (int i = 0; i < NI; ++i) v[e][i] = ok[i] ? __ldg(Ce + off[i]) : 0u;
+                Ce += inS;
             }
             __syncthreads();  // previous block's readers of Stg / stot are done
 #pragma unroll
