@@ -424,7 +424,10 @@ def gpu_arm(args) -> None:
                 "peak": round(pk, 3),
                 "unit": "T int32-lane-op/s",
                 "frac": round(achieved / pk, 4),
-                "traffic": committed_traffic(pl),
+                # dram__bytes_read + write per node-kernel launch (committed ncu --set full
+                # capture of this workload), details in traffic_detail
+                "traffic": (lambda tr: round(tr["dram_bytes_per_launch"]) if tr else None)(committed_traffic(pl)),
+                "traffic_detail": committed_traffic(pl),
                 "work_per_product": round(W, 1),
                 "work_model": "W_alg = 144 t^log2(3) + 4t (SURVEY §8(d)), t=ceil(n/64)",
                 "peak_source": "live LOP3 microbenchmark (c^(a&b), 8 chains/thread, 8 CTAs/SM) this run",
