@@ -385,58 +385,6 @@ __device__ __forceinline__ void node_level(uint4 *As, uint4 *Bs, const uint16_t 
     }
 }
 
-// Evaluation levels 2, 3 and 4 in one phase (KC = 5, F2X_EVAL_TRIPLE): item
-// (operand, level-2 node nu, quad v of a chunk) reads quad v of the node's 8
-// chunks and writes, from registers, the level-2 mid (4 chunks), the three
-// level-3 nodes' mids (2 chunks each) and the nine level-4 nodes' mids -- the
-// mid LEAVES' operands, stored at the chunk of the thread that multiplies
-// them (162 + minv[lambda], see kMidPerm).  Every leaf then finds both
-// operands in its own chunk pair, so the leaf phase needs no barrier and no
-// XOR-loading (the fused-bottom form needs two barriers and XORs a mid
-// leaf's a operand in both passes).
-template <int LF, int KC, int NTH>
-__device__ __forceinline__ void eval_triple2(uint4 *As, uint4 *Bs, const uint16_t *pos, const uint8_t *minv,
-                                             int t) {
-    using C = K2Cfg<LF, KC>;
-    static_assert(KC == 5, "eval_triple2 is the KC = 5 schedule");
-    constexpr int Q = C::Q;
-    constexpr int R3 = Q * 8 * 9;    // level-3 appended mids (quads): Q 2^(KC-2) 3^2
-    constexpr int R4 = Q * 4 * 27;   // level-4 appended mids: Q 2^(KC-3) 3^3
-    constexpr int R5 = Q * 2 * 81;   // leaf-level mids: Q 2^(KC-4) 3^4 (chunk 162)
-    const uint16_t *P2 = pos + 4;    // level-2 entries start at (3^2 - 1) / 2
-#pragma unroll 1
-    for (int it = t; it < 2 * 9 * Q; it += NTH) {
-        const int op = it >= 9 * Q;
-        const int r = it - op * 9 * Q;
-        const int nu = r / Q, v = r - nu * Q;
-        uint4 *X = op ? Bs : As;
-        const int p = int(P2[nu]) + v;
-        uint4 a[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] = X[p + k * Q];
-        uint4 m[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            m[k] = a[k] ^ a[k + 4];
-            X[R3 + nu * 4 * Q + k * Q + v] = m[k];
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const uint4 x0 = c == 0 ? a[0] : (c == 1 ? a[4] : m[0]);
-            const uint4 x1 = c == 0 ? a[1] : (c == 1 ? a[5] : m[1]);
-            const uint4 x2 = c == 0 ? a[2] : (c == 1 ? a[6] : m[2]);
-            const uint4 x3 = c == 0 ? a[3] : (c == 1 ? a[7] : m[3]);
-            const int mu = 3 * nu + c;
-            const uint4 y0 = x0 ^ x2, y1 = x1 ^ x3;
-            X[R4 + mu * 2 * Q + v] = y0;
-            X[R4 + mu * 2 * Q + Q + v] = y1;
-            X[R5 + int(minv[3 * mu]) * Q + v] = x0 ^ x1;
-            X[R5 + int(minv[3 * mu + 1]) * Q + v] = x2 ^ x3;
-            X[R5 + int(minv[3 * mu + 2]) * Q + v] = y0 ^ y1;
-        }
-    }
-}
-
 // Item -> (node nu, quad w) for a phase over NODES nodes of q quads each: the// Item -> (node nu, quad w) for a phase over NODES nodes of q quads each: the
 // first q & ~7 quads of every node are taken 8 at a time (an 8-thread shared
 // memory phase then touches 8 consecutive quads of ONE node: conflict-free),
@@ -552,9 +500,6 @@ __device__ __forceinline__ void interp_pair(uint4 *As, uint4 *Bs, const uint16_t
 #define F2X_FUSED_LOAD_EVAL 1
 #endif
 
-#ifndef F2X_EVAL_TRIPLE
-#define F2X_EVAL_TRIPLE 0  // measured slower; kept for experiments
-#endif
 
 #ifndef F2X_FUSED_STORE
 #define F2X_FUSED_STORE 1
@@ -564,11 +509,6 @@ __device__ __forceinline__ void interp_pair(uint4 *As, uint4 *Bs, const uint16_t
 #define F2X_FUSED_BOTTOM_EVAL 1
 #endif
 __host__ __device__ constexpr int kEvalLevels(int KC) { return F2X_FUSED_BOTTOM_EVAL ? KC - 1 : KC; }
-// levels 2-4 evaluated in one phase after the fused load + levels 0-1 (KC = 5)
-__host__ __device__ constexpr bool kEvalTriple(int KC) {
-    return F2X_EVAL_TRIPLE && F2X_FUSED_LOAD_EVAL && F2X_FUSED_BOTTOM_EVAL && KC == 5;
-}
-
 template <int LF, int KC, int NTH, int J, class Bar>
 __device__ __forceinline__ void node_eval_from(uint4 *As, uint4 *Bs, const uint16_t *pos, int t, Bar bar) {
     constexpr int NE = kEvalLevels(KC);  // levels 0..NE-1 evaluated here
@@ -988,31 +928,6 @@ __device__ __forceinline__ void node_leaves(uint4 *As, uint4 *Bs, const uint16_t
         }
         return;
     }
-    if constexpr (kEvalTriple(KC)) {
-        // every operand is in the leaf's own chunk pair (eval_triple2): no
-        // barriers, no XOR loads; products stored as soon as they are done
-        (void)pos;
-        (void)mperm;
-        (void)bar;
-        if (t < C::NLEAF) {
-            const int own = t * Q;
-            uint32_t b[LF], c[LF];
-            leaf_load_b<LF, Q, false>(Bs, own, own, false, b);
-            if constexpr (kLeafLoop(LF)) {
-                leaf_loop<LF, Q>(As, Bs, own, own, own, false, false, b, c);
-            } else {
-                leaf_passes<LF, Q, false>(As, Bs, own, own, own, false, b, c);
-            }
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                uint32_t o[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) o[r] = 4 * q + r < LF ? c[4 * q + r] : 0u;
-                As[own + q] = make_uint4(o[0], o[1], o[2], o[3]);
-            }
-        }
-        return;
-    }
     constexpr int RM = C::NLEAF - pow3c(KC - 1);  // first mid-leaf chunk
     const bool active = t < C::NLEAF;
     const bool mid = active && t >= RM;
@@ -1121,10 +1036,7 @@ k2_node_mul(const K2Params p, int64_t nodes) {
     if (KC == 5 && tid < 2 * 81) mtab[tid] = uint8_t(mt);
     __syncthreads();
     mark(1);
-    if constexpr (kEvalTriple(KC)) {
-        eval_triple2<LF, KC, C::NT>(As, Bs, pos, mtab + 81, tid);
-        __syncthreads();
-    } else if constexpr (kFuseEval0) {
+    if constexpr (kFuseEval0) {
         node_eval_from<LF, KC, C::NT, 2>(As, Bs, pos, tid, SyncAll{});
     } else {
         node_eval<LF, KC, C::NT>(As, Bs, pos, tid, SyncAll{});
