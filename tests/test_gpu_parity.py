@@ -359,7 +359,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("tl,seq", [(0, None), (1, None), (2, None), (3, None), (2, 1), (2, 10 ** 9)])
+@pytest.mark.parametrize("tl,seq", [(0, None), (1, None), (2, None), (3, None), (2, 1), (3, 1), (2, 10 ** 9)])
 def test_toom_levels_forced(tl, seq, cuda):
     """Toom-3 levels above the Karatsuba node problem (F2X_TOOM, read once per
     process): 0-3 levels give the oracle's bits for ring and full sizes,
