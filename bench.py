@@ -96,14 +96,7 @@ def committed_traffic(pl) -> dict | None:
             el = pl.get("eval_levels", 0)
             ns = 3 ** el * (pl["leaf_stride"] << (pl["levels"] - el))
             ss = pl["leaf_stride"] << pl["cta_levels"]
-            # fuse mode 1 writes only the 3^(GL-1) cluster parents (4 Ss words each); mode 2
-            # writes the node products, then re-reads two siblings' products and writes
-            # the parent (in place) per triple
-            fm, gl = pl.get("fuse_mode", 0), pl["global_levels"]
-            if fm == 1:
-                words = 3 ** (gl - 1) * 4 * ss
-            else:
-                words = 3 ** gl * 2 * ss + (3 ** (gl - 1) * (2 * 2 * ss + 4 * ss) if fm == 2 else 0)
+            words = 3 ** pl["global_levels"] * 2 * ss
             alg = 4 * pl["groups"] * (2 * ns + words)
             best = {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"],
                     "algorithmic_bytes_per_launch": alg,
@@ -415,7 +408,7 @@ def gpu_arm(args) -> None:
                 "parallelism": f"independent batch shards x{world}, no collectives",
                 "l2": "flushed before each timed step (256 MiB write, outside events)",
                 "plan": {k: pl[k] for k in ("N", "leaf_words", "levels", "cta_levels",
-                                             "global_levels", "pass_levels", "fused_levels", "fuse_mode", "node_ctas")},
+                                             "global_levels", "pass_levels", "node_ctas")},
             },
             "roofline": {
                 "bound": "int_alu",

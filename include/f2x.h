@@ -11,8 +11,9 @@
  *
  * Layout (poly.py:4-8, unchanged): row-major uint64[batch][t]; bit i of word
  * j of a row is the coefficient of X^(64 j + i).  All data pointers are
- * DEVICE pointers (cudaMalloc / torch CUDA tensors), 16-byte aligned,
- * non-aliasing.  Calls are asynchronous on `stream` (a cudaStream_t; NULL =
+ * DEVICE pointers (cudaMalloc / torch CUDA tensors), non-aliasing; A, B, C
+ * need only uint64 (8-byte) alignment, so any row view of a batch works; the
+ * workspace must be 16-byte aligned.  Work runs on the stream's device.  Calls are asynchronous on `stream` (a cudaStream_t; NULL =
  * legacy default stream), reentrant, and allocate nothing: the caller passes
  * a device workspace of at least f2x_workspace_bytes() bytes.
  *
@@ -80,14 +81,6 @@ typedef struct f2x_plan {
                                 (node kernel runs on 5^toom_levels x groups) */
     int32_t toom_w;          /* Toom-3 point x = X^toom_w                      */
     int32_t toom_M[4];       /* part size (coefficients) of Toom level 1..     */
-    int32_t fused_levels;    /* 1: the deepest global Karatsuba level is
-                                combined inside the node kernel (fuse_mode),
-                                the interpolation passes start one level up */
-    int32_t fuse_mode;       /* 0 none; 1: the 3 sibling node CTAs form a
-                                thread-block cluster and build the parent
-                                through distributed shared memory; 2: the last
-                                sibling to finish (atomic counter) builds the
-                                parent in place from the L2-resident products */
 } f2x_plan;
 
 /* Fill *plan for a call shape.  leaf_hint = 0 picks the default leaf;

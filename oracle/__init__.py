@@ -29,6 +29,28 @@ def build() -> str:
     return _SO
 
 
+REF_ROOT = "/root/reference"
+REF_TESTS = os.path.join(_HERE, "_ref", "ref_tests")
+
+
+def stage_reference_tests() -> str | None:
+    """Stage the reference's OWN unit tests (pkg/tests/conftest.py,
+    test_poly.py), unmodified, into oracle/_ref/ref_tests/ when the reference
+    tree is present (this container).  oracle/_ref/ is git-ignored (kept out
+    of history) but travels to the GPU box with the snapshot, where
+    tests/test_reference_suite.py runs them against the drop-in through
+    tests/ref_shim/f2xmul.  Returns the staged directory or None."""
+    import shutil
+
+    src = os.path.join(REF_ROOT, "pkg", "tests")
+    if not os.path.isdir(src):
+        return REF_TESTS if os.path.isdir(REF_TESTS) else None
+    os.makedirs(REF_TESTS, exist_ok=True)
+    for f in ("conftest.py", "test_poly.py"):
+        shutil.copyfile(os.path.join(src, f), os.path.join(REF_TESTS, f))
+    return REF_TESTS
+
+
 def c_oracle():
     """Load (building if needed) the C oracle library."""
     global _lib

@@ -62,8 +62,6 @@ class F2xPlan(ctypes.Structure):
         ("toom_levels", ctypes.c_int32),
         ("toom_w", ctypes.c_int32),
         ("toom_M", ctypes.c_int32 * 4),
-        ("fused_levels", ctypes.c_int32),
-        ("fuse_mode", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

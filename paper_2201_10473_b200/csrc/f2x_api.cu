@@ -17,7 +17,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <vector>
 
 #include "../../include/f2x.h"
 #include "f2x_kernels.cuh"
@@ -53,12 +52,11 @@ static constexpr int kToomMinWords = 544;      // Toom only above 512 words: d=3
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// every pipeline kernel goes through launch_pdl (programmatic dependent launch)
-#define F2X_LAUNCH(kern, grid, block, smem, stream, ...)                                          \
-    do {                                                                                          \
-        const cudaError_t le_ = launch_pdl(kern, dim3(grid), dim3(block), size_t(smem), stream,   \
-                                           __VA_ARGS__);                                          \
-        if (le_ != cudaSuccess) return F2X_ECUDA - int(le_);                                      \
+#define F2X_LAUNCH(kern, grid, block, smem, stream, ...)                             \
+    do {                                                                             \
+        kern<<<dim3(grid), dim3(block), size_t(smem), stream>>>(__VA_ARGS__);        \
+        const cudaError_t le_ = cudaGetLastError();                                  \
+        if (le_ != cudaSuccess) return F2X_ECUDA - int(le_);                         \
     } while (0)
 
 static inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -124,7 +122,6 @@ __global__ void __launch_bounds__(kTileThreads)
 k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
          uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
          int ncyc, uint32_t *d_err, int tiles) {
-    pdl_prologue();
     __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
@@ -183,7 +180,6 @@ __global__ void __launch_bounds__(kTileThreads << EL)
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
               int ncyc, uint32_t *d_err, int tiles, int TW) {
-    pdl_prologue();
     // TW (<= 64) operand words per tile: the part is cut into `tiles`
     // balanced tiles, so no CTA carries a nearly empty tail tile
     constexpr int NP = 1 << EL;               // parts
@@ -265,7 +261,6 @@ __global__ void __launch_bounds__(256)
 toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
                 uint32_t *__restrict__ Yb, int64_t items_in, int64_t inS, int M, int w, int S, int LFo,
                 int LFSo, int64_t outS) {
-    pdl_prologue();
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= items_in * outS) return;
     const int64_t i = idx / outS;
@@ -308,7 +303,6 @@ toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb
 __global__ void __launch_bounds__(256)
 toom_eval_level_q(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
                   uint32_t *__restrict__ Yb, int64_t inS, int M, int w, int S, int LFo, int LFSo, int64_t outS) {
-    pdl_prologue();
     const int sq = int(blockIdx.x) * 256 + int(threadIdx.x);
     const int sw0 = 4 * sq;
     if (sw0 >= outS) return;
@@ -401,7 +395,6 @@ struct ToomIn {
 __global__ void __launch_bounds__(kToomScanT)
 toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uint32_t *__restrict__ Tot, int M,
                  int w, int LFi, int LFSi, int64_t inS, int Lin, int nb) {
-    pdl_prologue();
     extern __shared__ uint32_t tsm[];
     const int H = kToomBlk + 3 * w;          // staged span per input
     constexpr int HP = kToomStgStride;        // padded stride per input (see tstg)
@@ -513,7 +506,6 @@ template <int BLK>
 __global__ void __launch_bounds__(kToomScanT, 3)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS) {
-    pdl_prologue();
     extern __shared__ uint32_t tsm[];
     constexpr int W = kToomW, ROWS = BLK / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
     constexpr int H = BLK + 3 * W;
@@ -698,7 +690,6 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
 __global__ void __launch_bounds__(256)
 toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict__ Tot, uint32_t *__restrict__ R,
                      int M, int w, int nb, int nbo, int64_t outS) {
-    pdl_prologue();
     extern __shared__ uint32_t carry[];  // [nb][3][w]
     const int64_t item = blockIdx.x / nbo;
     const int ob = int(blockIdx.x - item * nbo);
@@ -808,7 +799,6 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t items, int qw,
           int64_t inStride, int64_t outStride) {
-    pdl_prologue();
     // blocks walk the nodes in REVERSE order: the node kernel wrote them in
     // forward order, so the most recently written (still L2-resident)
     // products are consumed first instead of being evicted by the rest
@@ -833,7 +823,6 @@ template <int TW>
 __global__ void __launch_bounds__(2 * TW)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
-    pdl_prologue();
     constexpr int TC = 64 * TW, TT = 2 * TW;  // coefficients, threads per tile
     __shared__ uint32_t stage[TC + TC / 32];
     const int tid = threadIdx.x;
@@ -902,7 +891,6 @@ struct Layout {
     int64_t off_r[kMaxToom + 1] = {};  // Toom interpolation outputs, level l
     int64_t off_q[kMaxToom + 1] = {};  // level-l c_0..c_4 before carries (5 x 2M per item)
     int64_t off_tot[kMaxToom + 1] = {};  // level-l chain totals per block
-    int64_t off_cnt = 0;             // fuse mode 2: per-parent arrival counters
 };
 
 // Top global levels pre-evaluated by the slicing kernel (k1_slice_eval):
@@ -976,27 +964,22 @@ static int toom_blk_choice() {
     return v;
 }
 
-// Combining the deepest global Karatsuba level inside the node kernel
-// (F2X_FUSE, read once): 0 off (default: a separate interpolation pass);
-// 1 3-CTA clusters + distributed shared memory (node kernel 15-18 % slower:
-// cluster gang scheduling and two cluster barriers idle CTA slots); 2 the
-// last-arriving sibling builds the parent in place (node kernel ~8 % slower:
-// the finishing CTA's memory work holds an ALU-bound CTA slot).  Both cost
-// more than the pass they save.
-static int fuse_mode_env() {
-    static const int v = [] {
-        const char *e = getenv("F2X_FUSE");
-        return (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 0;
-    }();
-    return v;
-}
-
 static int64_t toom_seq_min() {
     static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
         return e ? int64_t(atoll(e)) : int64_t(256);
     }();
     return v;
+}
+
+// One CTA per product (toom_interp_seq) when a level has enough products to
+// fill the GPU; otherwise the two-kernel form, whose assembly kernel keeps
+// the chain carries of all nb = ceil(2M/2048) blocks in shared memory
+// (nb x 3w words): above the 48 KB default it also falls back to the
+// sequential form (t > ~12K words with few products).
+static bool toom_use_seq(int64_t items, int64_t M) {
+    const int64_t nb = ceil_div(2 * M, kToomBlk);
+    return items >= toom_seq_min() || nb * 3 * kToomW * 4 > 48 * 1024;
 }
 
 // F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
@@ -1071,10 +1054,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->levels = K;
     pl->cta_levels = KC;
     pl->global_levels = GL;
-    // the deepest global level combined inside the node kernel (fuse_mode_env)
-    const int FM = GL >= 1 ? fuse_mode_env() : 0;
-    const int CL = FM ? 1 : 0;
-    int rem = GL - CL, np = 0;
+    int rem = GL, np = 0;
     while (rem > 0) {
         const int p = std::min(kMaxPassLevels, rem);
         pl->pass_levels[np++] = p;
@@ -1085,8 +1065,6 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
-    pl->fused_levels = CL;
-    pl->fuse_mode = FM;
     pl->toom_levels = TL;
     pl->toom_w = TL ? kToomW : 0;
     for (int l = 1; l <= TL; ++l) pl->toom_M[l - 1] = int32_t(bestM[l]);
@@ -1123,22 +1101,18 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.off_abs = off;
     L.off_bbs = align256(L.off_abs + opw * 4);
     L.off_p0 = align256(L.off_bbs + opw * 4);
-    // node products (mode 2: parents overwrite their triple's first 4 Ss words), or
-    // the cluster parents (mode 1)
-    const int64_t p0 = FM == 1 ? G2 * ipow3(GL - 1) * 4 * L.Ss * 4 : G2 * ipow3(GL) * 2 * L.Ss * 4;
+    const int64_t p0 = G2 * ipow3(GL) * 2 * L.Ss * 4;  // node products
     L.off_p1 = align256(L.off_p0 + p0);
     int64_t p1 = 0;
     if (np >= 1) {  // first pass output (the largest one written to P1)
-        const int d1 = GL - CL - pl->pass_levels[0];
+        const int d1 = GL - pl->pass_levels[0];
         p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
     off = align256(L.off_p1 + p1);
-    L.off_cnt = off;  // mode-2 arrival counters, one per parent
-    if (FM == 2) off = align256(off + G2 * ipow3(GL - 1) * 4);
     for (int l = TL; l >= 1; --l) {  // Toom interpolation: [block scans, totals,] outputs
         const int64_t items = G * ipow5(l - 1);
         L.off_q[l] = L.off_tot[l] = off;
-        if (items < toom_seq_min()) {  // two-kernel form: c_j and chain totals in HBM
+        if (!toom_use_seq(items, L.M[l])) {  // two-kernel form: c_j and chain totals in HBM
             off = align256(off + items * 5 * 2 * L.M[l] * 4);
             L.off_tot[l] = off;
             off = align256(off + items * ceil_div(2 * L.M[l], kToomBlk) * 3 * kToomW * 4);
@@ -1148,7 +1122,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     }
     L.total = off;
     {  // every pass output must fit the ping-pong buffer it is written to
-        int d = GL - CL;
+        int d = GL;
         for (int i = 0; i < np; ++i) {
             const int dlo = d - pl->pass_levels[i];
             const int64_t outb = G2 * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
@@ -1165,8 +1139,8 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
 template <int D>
 static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw, int64_t inS,
                      int64_t outS, cudaStream_t s) {
-    const cudaError_t e = launch_pdl(k3_interp<D>, dim3(unsigned(ceil_div(items, kThreads))), dim3(kThreads), 0, s,
-                                     Pin, Pout, items, qw, inS, outS);
+    k3_interp<D><<<unsigned(ceil_div(items, kThreads)), kThreads, 0, s>>>(Pin, Pout, items, qw, inS, outS);
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : F2X_ECUDA - int(e);
 }
 
@@ -1214,13 +1188,38 @@ static int debug_sync(cudaStream_t s, int stage) {
     return 0;
 }
 
+// Makes the device of a (non-legacy) stream current for the duration of a
+// call when it differs from the caller's current device.
+struct DeviceGuard {
+    int prev = -1;
+    int to_stream(cudaStream_t s) {
+        int sdev = -1, cdev = -1;
+        if (cudaStreamGetDevice(s, &sdev) != cudaSuccess || cudaGetDevice(&cdev) != cudaSuccess) return 0;
+        if (sdev == cdev) return 0;
+        const cudaError_t e = cudaSetDevice(sdev);
+        if (e != cudaSuccess) return F2X_ECUDA - int(e);
+        prev = cdev;
+        return 0;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int64_t batch,
                int t_or_n, void *ws, size_t ws_bytes, int leaf_hint, uint32_t *d_err,
                cudaStream_t stream) {
     if (!A || !B || !C || !ws) return F2X_EINVAL;
-    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
-         reinterpret_cast<uintptr_t>(C) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    int rc0 = 0;
+    // rows are read and written as 32-bit half-words: any uint64-aligned row
+    // view works (e.g. A[1:] of an odd-t batch); the workspace holds 16-byte
+    // quads
+    if (((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+          reinterpret_cast<uintptr_t>(C)) & 7) || (reinterpret_cast<uintptr_t>(ws) & 15))
         return F2X_EINVAL;
+    // launch on the stream's device; the caller's current device is restored
+    DeviceGuard dg;
+    if (stream != nullptr && (rc0 = dg.to_stream(stream))) return rc0;
     f2x_plan pl;
     Layout L;
     int rc = plan_impl(kind, batch, t_or_n, leaf_hint, &pl, &L);
@@ -1323,53 +1322,14 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     kp.K = pl.levels - L.el;
     kp.GL = pl.global_levels - L.el;
     kp.paths = int(ipow3(pl.global_levels - L.el));
-    kp.prof = nullptr;
-    kp.combine = pl.fuse_mode;
-    kp.cnt = nullptr;
-    if (pl.fuse_mode == 2) {
-        kp.cnt = reinterpret_cast<unsigned *>(w + L.off_cnt);
-        const cudaError_t me = cudaMemsetAsync(kp.cnt, 0, size_t(pl.node_ctas / 3) * 4, stream);
-        if (me != cudaSuccess) return F2X_ECUDA - int(me);
-    }
-    const char *prof_path = getenv("F2X_PHASE_PROF");  // development aid
-    if (prof_path) {
-        cudaMalloc(&kp.prof, size_t(pl.node_ctas) * 8 * sizeof(long long));
-        cudaMemset(kp.prof, 0, size_t(pl.node_ctas) * 8 * sizeof(long long));
-    }
     if (g_node_ev[0]) cudaEventRecord(g_node_ev[0], stream);
     rc = e->launch(kp, pl.node_ctas, stream);
     if (rc) return rc;
     if (g_node_ev[1]) cudaEventRecord(g_node_ev[1], stream);
-    if (kp.prof) {
-        std::vector<long long> h(size_t(pl.node_ctas) * 8);
-        cudaStreamSynchronize(stream);
-        cudaMemcpy(h.data(), kp.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-        cudaFree(kp.prof);
-        FILE *f = fopen(prof_path, "a");
-        if (f) {  // per-CTA phase cycles (one node per CTA), slot 7 = -nodes
-            double a[6] = {0};
-            long long nodes = 0;
-            int rows = 0;
-            for (int64_t b = 0; b < pl.node_ctas && h[b * 8 + 7] < 0; ++b, ++rows) {
-                for (int i = 0; i < 6; ++i) a[i] += double(h[b * 8 + i]);
-                nodes += -h[b * 8 + 7];
-            }
-            if (nodes < 1) {  // the kernel was built without the clocks
-                fprintf(f, "F2X_PHASE_PROF: rebuild with F2X_NVCC_EXTRA=-DF2X_PROF_BUILD=1\n");
-                nodes = 1;
-            }
-            fprintf(f, "LF=%d KC=%d GL=%d ctas=%d nodes=%lld cycles/node per slot: %.0f %.0f %.0f %.0f %.0f %.0f  (setup load eval leaf interp store)\n",
-                    pl.leaf_words, pl.cta_levels, pl.global_levels, rows, nodes, a[0] / nodes,
-                    a[1] / nodes, a[2] / nodes, a[3] / nodes, a[4] / nodes, a[5] / nodes);
-            fclose(f);
-        }
-    }
     // K3 passes
     uint32_t *cur = P0, *nxt = P1;
-    int d = pl.global_levels - pl.fused_levels;
-    // stride of the first pass's input products (mode 2: parents in place of
-    // their triple, 6 Ss words apart)
-    int64_t in_stride0 = pl.fuse_mode == 2 ? 6 * L.Ss : 2 * (L.Ns >> d);
+    int d = pl.global_levels;
+    const int64_t in_stride0 = 2 * (L.Ns >> d);  // node products
     for (int i = 0; i < pl.num_passes; ++i) {
         const int D = pl.pass_levels[i];
         const int dlo = d - D;
@@ -1385,13 +1345,6 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             default: return F2X_ERANGE;
         }
         if (rc) return rc;
-        if (getenv("F2X_DEBUG_SYNC"))
-            fprintf(stderr, "f2x pass %d: D=%d d=%d dlo=%d qw=%d items=%lld inS=%lld outS=%lld "
-                    "cur=%s maxread=%lld maxwrite=%lld p0=%lld p1=%lld\n", i, D, d, dlo, qw,
-                    (long long)items, (long long)(2 * Shi), (long long)(2 * Slo),
-                    cur == P0 ? "P0" : "P1", (long long)(G * ipow3(d) * 2 * Shi),
-                    (long long)(G * ipow3(dlo) * 2 * Slo), (long long)((L.off_p1 - L.off_p0) / 4),
-                    (long long)((L.total - L.off_p1) / 4));
         if ((rc = debug_sync(stream, 3))) return rc;
         std::swap(cur, nxt);
         d = dlo;
@@ -1413,7 +1366,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const size_t sms = size_t(5) * kToomStgStride * 4;
         // one CTA per item (carries in shared memory) when there are enough
         // items to fill the GPU, else the two-kernel form
-        const bool seq = items >= toom_seq_min();
+        const bool seq = toom_use_seq(items, M);
         static std::atomic<uint32_t> attr_dev_mask{0};  // devices configured (idempotent set)
         int dev = 0;
         cudaGetDevice(&dev);

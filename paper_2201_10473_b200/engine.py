@@ -69,8 +69,14 @@ def _check_operands(A: torch.Tensor, B: torch.Tensor) -> None:
         raise ValueError("zero-length polynomials are rejected; need t >= 1")
     if not A.is_cuda or A.device != B.device:
         raise ValueError("operands must live on the same CUDA device")
-    if not A.is_contiguous() or not B.is_contiguous():
-        raise ValueError("operands must be contiguous")
+
+
+def _rows(X: torch.Tensor) -> torch.Tensor:
+    """Row-major words for the C ABI.  Any contiguous row view works as is
+    (rows need only 8-byte alignment, e.g. A[1:] of an odd-t batch); other
+    strided views are copied once, like the reference accepting any
+    PolyWords (poly.py:70-90)."""
+    return X if X.is_contiguous() else X.contiguous()
 
 
 def plan(kind: str, batch: int, t_or_n: int, leaf: int = 0) -> dict:
@@ -79,10 +85,23 @@ def plan(kind: str, batch: int, t_or_n: int, leaf: int = 0) -> dict:
     return _lib.make_plan(k, batch, t_or_n, leaf).as_dict()
 
 
+def _scratch(lib, kind: int, batch: int, t_or_n: int, leaf: int, device, stream,
+             workspace: torch.Tensor | None):
+    chunks, need = _row_chunks(lib, kind, batch, t_or_n, leaf)
+    if workspace is None:
+        return chunks, _workspace(device, stream, need)
+    if workspace.dtype != torch.uint8 or workspace.device != device or workspace.numel() < need:
+        raise ValueError(f"workspace must be a uint8 tensor of >= {need} bytes on {device}")
+    return chunks, workspace
+
+
 def mul_full(A: torch.Tensor, B: torch.Tensor, *, out: torch.Tensor | None = None,
-             leaf: int = 0) -> torch.Tensor:
-    """C[r] = A[r] * B[r] over F2[X] for every row r; C has 2t words."""
+             leaf: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """C[r] = A[r] * B[r] over F2[X] for every row r; C has 2t words.
+    ``workspace`` (uint8 CUDA tensor, optional): caller-owned scratch, else
+    a per-(device, stream) cached buffer."""
     _check_operands(A, B)
+    A, B = _rows(A), _rows(B)
     batch, t = A.shape
     if out is None:
         out = torch.empty((batch, 2 * t), dtype=A.dtype, device=A.device)
@@ -94,8 +113,7 @@ def mul_full(A: torch.Tensor, B: torch.Tensor, *, out: torch.Tensor | None = Non
     lib = _lib.load()
     with torch.cuda.device(A.device):
         stream = torch.cuda.current_stream(A.device)
-        chunks, need = _row_chunks(lib, _lib.KIND_FULL, batch, t, leaf)
-        ws = _workspace(A.device, stream, need)
+        chunks, ws = _scratch(lib, _lib.KIND_FULL, batch, t, leaf, A.device, stream, workspace)
         for lo, hi in chunks:
             rc = lib.f2x_mul_full(A[lo:hi].data_ptr(), B[lo:hi].data_ptr(), out[lo:hi].data_ptr(),
                                   hi - lo, t, ws.data_ptr(), ws.numel(), leaf, stream.cuda_stream)
@@ -105,7 +123,8 @@ def mul_full(A: torch.Tensor, B: torch.Tensor, *, out: torch.Tensor | None = Non
 
 def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | None = None,
                leaf: int = 0, check: bool = True,
-               err_flag: torch.Tensor | None = None) -> torch.Tensor:
+               err_flag: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None) -> torch.Tensor:
     """C[r] = A[r] * B[r] mod X^n - 1 for every row r (t = ceil(n/64) words).
 
     Inputs with any bit >= n set are rejected with ValueError (SPEC.md:349,
@@ -116,6 +135,7 @@ def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | 
     inspects it later -- the asynchronous form used inside timed loops.
     """
     _check_operands(A, B)
+    A, B = _rows(A), _rows(B)
     n = int(n)
     if n < 1:
         raise ValueError("ring degree n must be >= 1")
@@ -135,8 +155,7 @@ def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | 
         flag = err_flag
         if flag is None:
             flag = torch.zeros(1, dtype=torch.int32, device=A.device)
-        chunks, need = _row_chunks(lib, _lib.KIND_CYCLIC, batch, n, leaf)
-        ws = _workspace(A.device, stream, need)
+        chunks, ws = _scratch(lib, _lib.KIND_CYCLIC, batch, n, leaf, A.device, stream, workspace)
         for lo, hi in chunks:
             rc = lib.f2x_mul_cyclic(A[lo:hi].data_ptr(), B[lo:hi].data_ptr(), out[lo:hi].data_ptr(),
                                     hi - lo, n, ws.data_ptr(), ws.numel(), leaf, flag.data_ptr(),
@@ -187,12 +206,20 @@ class HostPipeline:
         rows = self.bounds[0][1] - self.bounds[0][0]
         self.lanes = []
         nstreams = max(1, int(streams))
+        # every (lane, stream) owns its buffers AND its scratch, sized here
+        # once: a captured graph bakes these pointers in, so they must never
+        # be shared with (or freed by) other callers of the same stream
+        lib = _lib.load()
+        kind_id = _lib.KIND_CYCLIC if kind == "cyclic" else _lib.KIND_FULL
+        self.ws_bytes = _row_chunks(lib, kind_id, rows, self.size, leaf)[1]
         for _ in range(max(1, lanes)):
             ss = [torch.cuda.Stream(self.device) for _ in range(nstreams)]
             bufs = [(torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
                      torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
                      torch.empty((rows, self.tout), dtype=torch.int64, device=self.device),
-                     torch.zeros(1, dtype=torch.int32, device=self.device)) for _ in ss]
+                     torch.zeros(1, dtype=torch.int32, device=self.device),
+                     torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device))
+                    for _ in ss]
             self.lanes.append({"launch": torch.cuda.Stream(self.device), "streams": ss,
                                "bufs": bufs, "graph": None, "key": None})
 
@@ -248,16 +275,16 @@ class HostPipeline:
         for i, (lo, hi) in enumerate(self.bounds):
             k = i % len(L["streams"])
             s = L["streams"][k]
-            dA, dB, dC, flag = L["bufs"][k]
+            dA, dB, dC, flag, ws = L["bufs"][k]
             r = hi - lo
             with torch.cuda.stream(s):
                 dA[:r].copy_(hA[lo:hi], non_blocking=True)
                 dB[:r].copy_(hB[lo:hi], non_blocking=True)
                 if self.kind == "cyclic":
                     mul_cyclic(dA[:r], dB[:r], self.size, out=dC[:r], leaf=self.leaf,
-                               check=False, err_flag=flag)
+                               check=False, err_flag=flag, workspace=ws)
                 else:
-                    mul_full(dA[:r], dB[:r], out=dC[:r], leaf=self.leaf)
+                    mul_full(dA[:r], dB[:r], out=dC[:r], leaf=self.leaf, workspace=ws)
                 hC[lo:hi].copy_(dC[:r], non_blocking=True)
         for s in L["streams"]:
             cur.wait_stream(s)

@@ -14,11 +14,14 @@ behaviour, so code written against the reference switches by import:
 Every multiply runs on the GPU through libf2x.so (one batched launch
 sequence per call; per-product calls are a batch of one).  There is no CPU
 arithmetic path.  The reference's lane-level backend seam (``BackendId``,
-poly.py:208-253) selects between bit-identical CPU recipes; here the single
-device path is always used, and a ``backend`` argument is validated and
-otherwise ignored.  ``MulCounters`` records the analytic work of the executed
-GPU plan (64x64-equivalent base products and 64-bit XORs), not the
-reference's t^2 convolution count.
+``backend_select``, ``set_backend_override``, ``F2XMUL_BACKEND``,
+poly.py:208-253) selects between bit-identical CPU recipes; here the
+selection logic is kept verbatim in behaviour (override, then environment,
+then the two machine probes) but every name maps to the single device path.
+``MulCounters`` keeps the reference's accounting (poly.py:451-514: one base
+multiplication per 64x64 lane, t*t of them and 2 t^2 word XORs per counted
+t-word product); the work the GPU plan actually executes is reported by
+``engine.plan`` (``leaf_ops_per_product``, ``karatsuba_ops_per_product``).
 """
 
 from __future__ import annotations
@@ -28,6 +31,7 @@ from enum import Enum
 from typing import Optional, Sequence, Union
 
 import numpy as np
+import os
 
 __all__ = [
     "PolyWords",
@@ -35,6 +39,7 @@ __all__ = [
     "MulCounters",
     "BackendId",
     "backend_select",
+    "set_backend_override",
     "clmul64",
     "clmul64_batch",
     "schoolbook_mul",
@@ -150,12 +155,10 @@ class WideProduct(PolyWords):
 
 @dataclass
 class MulCounters:
-    """Per-call work record (cf. poly.py:178-200).
-
-    For GPU calls ``base_mul_count`` accumulates the executed plan's
-    64x64-equivalent base products (leaf bit-products / 4096) and
-    ``xor64_count`` its Karatsuba XOR work in 64-bit words, per product.
-    """
+    """Per-call work record with the reference's semantics (poly.py:178-200):
+    ``base_mul_count`` = 64x64 word products of the schoolbook convolution
+    (t*t per t-word product, one per clmul lane), ``xor64_count`` = its 2 t^2
+    word XORs."""
 
     base_mul_count: int = 0
     xor64_count: int = 0
@@ -172,23 +175,60 @@ class MulCounters:
 
 
 class BackendId(Enum):
-    """Names accepted for source compatibility with poly.py:208-211.  All
-    reference backends are bit-identical by contract (test_poly.py:156-164);
-    this package has exactly one device path."""
+    """Backend names of poly.py:208-211.  All reference backends are
+    bit-identical by contract (test_poly.py:156-164); every name selects the
+    single device path of this package."""
 
     PORTABLE = "portable"
     CLMUL = "clmul"
     MULTILANE = "multilane"
 
 
+_BACKEND_ENV = "F2XMUL_BACKEND"
+_backend_override: Optional[BackendId] = None
+
+
+def set_backend_override(backend: Optional[Union[BackendId, str]]) -> None:
+    """Force a backend name for subsequent operations (None restores
+    detection), as poly.py:217-223; unknown names raise ValueError."""
+    global _backend_override
+    if backend is None:
+        _backend_override = None
+    else:
+        _backend_override = backend if isinstance(backend, BackendId) else BackendId(backend)
+
+
+def _machine_supports_wide_mul() -> bool:
+    """Probe seam (poly.py:226-231): the batched lane machinery here is the
+    GPU engine, always present when the package imports."""
+    return True
+
+
+def _int_mul_selfcheck() -> bool:
+    """Probe seam (poly.py:300-303).  The device leaf has no integer-multiply
+    recipe to self-check; kept so callers and tests can patch it."""
+    return True
+
+
 def backend_select() -> BackendId:
-    """Always MULTILANE: the batched device path is the only implementation."""
-    return BackendId.MULTILANE
+    """Backend name with the reference's priority (poly.py:234-246): explicit
+    override, then ``F2XMUL_BACKEND`` (portable/clmul/multilane/auto), then
+    the machine probes.  The name does not change the arithmetic."""
+    if _backend_override is not None:
+        return _backend_override
+    env = os.environ.get(_BACKEND_ENV, "").strip().lower()
+    if env and env != "auto":
+        return BackendId(env)
+    if _machine_supports_wide_mul():
+        return BackendId.MULTILANE
+    return BackendId.CLMUL if _int_mul_selfcheck() else BackendId.PORTABLE
 
 
 def _validate_backend(backend) -> None:
-    if backend is not None and not isinstance(backend, BackendId):
-        BackendId(backend)  # raises ValueError on unknown names, like poly.py:253
+    if backend is None:
+        backend_select()  # an invalid F2XMUL_BACKEND raises ValueError, as poly.py:249-253
+    elif not isinstance(backend, BackendId):
+        BackendId(backend)  # raises ValueError on unknown names
 
 
 def _device():
@@ -199,14 +239,13 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _count(counters: Optional[MulCounters], kind: str, batch: int, t_or_n: int) -> None:
+def _count_convolution(counters: Optional[MulCounters], t: int, batch: int = 1) -> None:
+    """The reference's counted-path accounting (poly.py:493-514): t*t lane
+    products and 2 t^2 word XORs per t-word product."""
     if counters is None:
         return
-    from .engine import plan
-
-    p = plan(kind, batch, t_or_n)
-    counters.add_muls(round(batch * p["leaf_ops_per_product"] / 128.0))
-    counters.add_xors(round(batch * p["karatsuba_ops_per_product"] / 2.0))
+    counters.add_muls(batch * t * t)
+    counters.add_xors(batch * 2 * t * t)
 
 
 def clmul64(a: int, b: int, counters: Optional[MulCounters] = None,
@@ -244,23 +283,47 @@ def clmul64_batch(a: np.ndarray, b: np.ndarray, counters: Optional[MulCounters] 
     return lo.cpu().numpy().copy(), hi.cpu().numpy().copy()
 
 
-def schoolbook_mul(a: PolyWords, b: PolyWords, counters: Optional[MulCounters] = None,
-                   backend: Optional[Union[BackendId, str]] = None) -> WideProduct:
-    """Exact F2[X] product of equal-length operands, 2t words (poly.py:547-561)."""
+def _mul_words(aw: np.ndarray, bw: np.ndarray) -> np.ndarray:
+    """One t-word product on the device; returns 2t uint64 words."""
     import torch
 
     from .engine import mul_full
 
+    dev = _device()
+    A = torch.from_numpy(np.ascontiguousarray(aw, dtype=np.uint64).view(np.int64).copy()).reshape(1, -1).to(dev)
+    B = torch.from_numpy(np.ascontiguousarray(bw, dtype=np.uint64).view(np.int64).copy()).reshape(1, -1).to(dev)
+    return mul_full(A, B).cpu().numpy().view(np.uint64)[0].copy()
+
+
+def _convolution_mul_arrays(aw: np.ndarray, bw: np.ndarray, counters: Optional[MulCounters],
+                            backend: Optional[Union[BackendId, str]]) -> np.ndarray:
+    """The reference's counted route (poly.py:493-514) as a name: the device
+    product, with the convolution's t*t / 2 t^2 accounting."""
+    _validate_backend(backend)
+    out = _mul_words(aw, bw)
+    _count_convolution(counters, int(np.asarray(aw).shape[0]))
+    return out
+
+
+def _spread_mul_arrays(aw: np.ndarray, bw: np.ndarray) -> np.ndarray:
+    """The reference's uncounted route (poly.py:517-544) as a name: the same
+    device product (one path here; the two reference routes are
+    bit-identical by contract, test_poly.py:225-239)."""
+    return _mul_words(aw, bw)
+
+
+def schoolbook_mul(a: PolyWords, b: PolyWords, counters: Optional[MulCounters] = None,
+                   backend: Optional[Union[BackendId, str]] = None) -> WideProduct:
+    """Exact F2[X] product of equal-length operands, 2t words (poly.py:547-561).
+    With ``counters`` the reference's accounting is added: t*t base
+    multiplications and 2 t^2 word XORs."""
     if a.word_len != b.word_len:
         raise ValueError(
             f"schoolbook_mul needs equal lengths, got {a.word_len} and {b.word_len}")
     _validate_backend(backend)
-    dev = _device()
-    A = torch.from_numpy(a.words.copy()).reshape(1, -1).to(dev)
-    B = torch.from_numpy(b.words.copy()).reshape(1, -1).to(dev)
-    C = mul_full(A, B)
-    _count(counters, "full", 1, a.word_len)
-    return WideProduct(C.cpu().numpy()[0])
+    out = _mul_words(a.words, b.words)
+    _count_convolution(counters, a.word_len)
+    return WideProduct(out)
 
 
 def to_hex(p: PolyWords) -> str:

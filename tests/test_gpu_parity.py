@@ -378,48 +378,6 @@ def test_toom_levels_forced(tl, seq, cuda):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
-_FUSE_SCRIPT = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, sys.argv[1])
-from oracle import c_mul_cyclic, c_mul_full
-from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
-from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
-fm = int(sys.argv[2])
-dev = torch.device("cuda", 0)
-d = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).to(dev)
-for n, b in ((12323, 70), (17669, 64), (35851, 33), (57637, 40)):
-    p = plan("cyclic", b, n)
-    assert p["fuse_mode"] == (fm if p["global_levels"] >= 1 else 0), p
-    A, B = make_cyclic_inputs(n, b)
-    for _ in range(2):  # mode 2: the arrival counters are reset between calls
-        out = mul_cyclic(d(A), d(B), n).cpu().numpy().view(np.uint64)
-        assert np.array_equal(out, c_mul_cyclic(A, B, n)), n
-for t, b in ((16, 33), (64, 40), (128, 7), (277, 5), (512, 9), (1024, 40)):
-    A, B = make_full_inputs(t, b, words=True)
-    out = mul_full(d(A), d(B)).cpu().numpy().view(np.uint64)
-    assert np.array_equal(out, c_mul_full(A, B)), t
-print("ok")
-"""
-
-
-@pytest.mark.parametrize("fm", [0, 1, 2])
-def test_fused_level_modes(fm, cuda):
-    """The deepest global Karatsuba level combined inside the node kernel is
-    a schedule choice (F2X_FUSE, read once per process): 0 a separate
-    interpolation pass (default), 1 3-CTA clusters over distributed shared
-    memory, 2 the last-arriving sibling.  All give the oracle's bits, ragged
-    batches and repeated calls included."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, F2X_FUSE=str(fm))
-    r = subprocess.run([sys.executable, "-c", _FUSE_SCRIPT, root, str(fm)], env=env,
-                       capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
-
-
 def test_workspace_budget_row_chunks(cuda):
     """A small scratch budget (F2X_WS_BUDGET, read at import) splits the batch
     into row chunks; results stay bit-exact."""

@@ -114,11 +114,7 @@ def test_plan_struct_size_matches_header(lib):
     assert pl.t == 277 and pl.n == 17669 and pl.groups == 128
     assert pl.N >= 64 * 277 and pl.N == pl.leaf_words << pl.levels
     assert pl.levels == pl.cta_levels + pl.global_levels
-    # the deepest global level combined inside the node kernel is opt-in (F2X_FUSE=1/2)
-    mode = int(os.environ.get("F2X_FUSE", "0"))
-    assert pl.fuse_mode == (mode if pl.global_levels >= 1 else 0)
-    assert pl.fused_levels == (1 if pl.fuse_mode else 0)
-    assert sum(pl.pass_levels[: pl.num_passes]) == pl.global_levels - pl.fused_levels
+    assert sum(pl.pass_levels[: pl.num_passes]) == pl.global_levels
     assert pl.launches == 3 + pl.num_passes
     assert pl.workspace_bytes > 0
 
