@@ -2,16 +2,29 @@
 
 Contract (one JSON line on rank 0):
   python bench.py --gpus N --steps K --warmup W [--impl reference]
-  N>1: torchrun --nproc-per-node N ... bench.py --gpus N ...
+  N > 1 either under torchrun (one process per GPU, RANK/WORLD_SIZE/LOCAL_RANK
+  from the env) or, with WORLD_SIZE unset, N worker processes spawned here
+  (worker r on cuda:r).  Ranks share no data: the only coordination is a
+  host-side barrier and a max over ranks of the timings (gloo over TCP under
+  torchrun, a multiprocessing barrier + shared array when spawned) -- no
+  NCCL, no collective on the data path (north_star).
 
-Workload (BASELINE.json configs[1]): hqc-128 ring multiplication
+Headline (BASELINE.json configs[1]): hqc-128 ring multiplication
 A*B mod X^17669 - 1, t = 277 uint64 words per operand, 4096 products per GPU
 per step (weak scaling: rank r owns rows [4096 r, 4096 (r+1)) of one seeded
-global batch; shards are independent -- no collective on the data path).
-A step = one call of the engine on a device-resident batch; inputs are seeded
-synthetic operands with i.i.d. uniform bits (SURVEY.md §8(d) generator) --
-no public dataset is involved.  L2 is flushed (256 MiB write) before every
-timed step; flushes are outside the per-step CUDA events.
+global batch), identical for every N.  A step = one call of the engine on a
+device-resident batch; inputs are seeded synthetic operands with i.i.d.
+uniform bits (SURVEY.md §8(d) generator) -- no public dataset is involved.
+L2 is flushed (256 MiB write) before every timed step; flushes are outside
+the per-step CUDA events.
+
+Also reported: ``scaling_57637`` (configs[3]: n=57637 x 16384 products split
+16384/N across the N GPUs, strong scaling) and, at N=1, ``per_config`` lines
+for configs[0] (n=12323 x 256), configs[2] (n=35851 x 4096), configs[3] and
+the configs[4] full-product d-sweep (~1 GB of operands per size).  Every
+timed output is checked against the C oracle outside the timed region on a
+stated row subsample (>= 256 rows incl. the first and last 32-row groups):
+``parity: {rows_checked, ok}``.
 
 --impl reference times the reference's CPU path (the oracle port of
 schoolbook_mul's default route, poly.py:517-561, plus the SPEC fold) on the
@@ -37,7 +50,10 @@ UNIT = "products/s"
 N_RING = 17669
 BATCH_PER_GPU = 4096
 L2_FLUSH_BYTES = 256 << 20
-EXTRA_CONFIGS = ((35851, 4096), (57637, 16384))
+RING_CONFIGS = ((12323, 256, "configs[0]"), (35851, 4096, "configs[2]"), (57637, 16384, "configs[3]"))
+SCALE_N, SCALE_BATCH = 57637, 16384
+DSWEEP = (1024, 4096, 8192, 16384, 32768, 65536)
+DSWEEP_OPERAND_BYTES = 1 << 30  # A + B per GPU
 
 
 def w_alg(t: int, cyclic: bool = True) -> float:
@@ -104,11 +120,100 @@ def committed_traffic(pl) -> dict | None:
     return best
 
 
+def split_rows(rank: int, world: int, total: int) -> slice:
+    """Strong scaling: rank r's contiguous share of `total` rows, cut on whole
+    32-row groups (the engine's bitsliced unit), balanced to within a group."""
+    if not 0 <= rank < world:
+        raise ValueError("rank outside [0, world)")
+    groups = -(-total // 32)
+    lo = (groups * rank // world) * 32
+    hi = min(total, (groups * (rank + 1) // world) * 32)
+    return slice(lo, hi)
+
+
+def parity_rows(batch: int, want: int = 256) -> "list[int]":
+    """Rows checked against the oracle: all rows when batch <= want, else the
+    first and the last 32-row groups plus an even stride through the rest."""
+    if batch <= want:
+        return list(range(batch))
+    edge = list(range(32)) + list(range(batch - 32, batch))
+    mid = want - len(edge)
+    step = (batch - 64) / mid
+    rows = set(edge) | {32 + int(i * step) for i in range(mid)}
+    return sorted(rows)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+class LocalSync:
+    """World of one."""
+
+    rank, world = 0, 1
+
+    def barrier(self):
+        pass
+
+    def max(self, vals):
+        return list(vals)
+
+    def close(self):
+        pass
+
+
+class GlooSync:
+    """torchrun ranks: host-side barrier and max over a gloo (TCP) group --
+    timing coordination only, no NCCL and no device data."""
+
+    def __init__(self, rank, world):
+        import torch.distributed as dist
+
+        self.dist, self.rank, self.world = dist, rank, world
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def barrier(self):
+        self.dist.barrier()
+
+    def max(self, vals):
+        import torch
+
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def close(self):
+        self.dist.destroy_process_group()
+
+
+class SpawnSync:
+    """Workers spawned by bench.py itself: a multiprocessing barrier and a
+    shared array of per-rank slots for the max over ranks."""
+
+    SLOTS = 32
+
+    def __init__(self, rank, world, barrier, arr):
+        self.rank, self.world, self._b, self._a = rank, world, barrier, arr
+
+    def barrier(self):
+        self._b.wait()
+
+    def max(self, vals):
+        vals = [float(v) for v in vals]
+        assert len(vals) <= self.SLOTS
+        base = self.rank * self.SLOTS
+        for i, v in enumerate(vals):
+            self._a[base + i] = v
+        self._b.wait()
+        out = [max(self._a[r * self.SLOTS + i] for r in range(self.world)) for i in range(len(vals))]
+        self._b.wait()  # nobody overwrites a slot before every rank has read it
+        return out
+
+    def close(self):
+        pass
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -126,7 +231,7 @@ def _ref_rows(args):
     return hi - lo, time.perf_counter() - t0
 
 
-def cpu_reference(n: int, rows_per_core: int = 48, pool=None, c_port: bool = True) -> dict:
+def cpu_reference(n: int, rows_per_core: int = 120, pool=None, c_port: bool = True) -> dict:
     """Reference CPU path on all host cores: the oracle's restatement of
     schoolbook_mul's default (bit-spread big-int) route + SPEC fold, one
     product per row (the reference has no batched API), processes because
@@ -257,31 +362,194 @@ def int_alu_peak(torch, lib, dev) -> dict:
     return {"ops_per_s": ops / sec, "sms": sms, "sec": sec}
 
 
-def gpu_arm(args) -> None:
+def check_rows(np, kind, size, hA, hB, dC, rows) -> dict:
+    """Oracle check of the timed output on `rows` (host copies of the inputs
+    of exactly those rows; the output rows are read back from the device)."""
+    from oracle import c_mul_cyclic, c_mul_full
+
+    idx = np.asarray(rows, dtype=np.int64)
+    A = np.ascontiguousarray(hA[idx])
+    B = np.ascontiguousarray(hB[idx])
+    import torch
+
+    got = dC[torch.from_numpy(idx).to(dC.device)].cpu().numpy().view(np.uint64)
+    want = c_mul_cyclic(A, B, size) if kind == "cyclic" else c_mul_full(A, B)
+    return {"rows_checked": int(idx.size), "ok": bool(np.array_equal(got, want)),
+            "rows": "all" if idx.size == hA.shape[0] else
+            "first+last 32-row groups + even stride (%d of %d)" % (idx.size, hA.shape[0])}
+
+
+def device_words(torch, batch, t, seed, dev):
+    """Uniform random uint64 words [batch][t] (as int64) generated on the
+    device from a seeded generator (the ~1 GB d-sweep inputs)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    return torch.randint(-2 ** 31, 2 ** 31, (batch, 2 * t), dtype=torch.int32, device=dev,
+                         generator=g).view(torch.int64)
+
+
+def time_calls(torch, fn, reps, warmup, flush) -> float:
+    """Mean device ms per call: CUDA events around each call on the current
+    stream, 256 MiB L2 flush before each (outside the events)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = []
+    for i in range(reps):
+        flush.fill_(i)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / reps
+
+
+def ring_entry(torch, np, dev, n, batch, label, peak, flush, reps=5, warmup=3) -> dict:
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200.engine import mul_cyclic, plan as eng_plan
+
+    A, B = make_cyclic_inputs(n, batch)
+    dA = torch.from_numpy(A.view(np.int64)).to(dev)
+    dB = torch.from_numpy(B.view(np.int64)).to(dev)
+    dC = torch.empty_like(dA)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    ms = time_calls(torch, lambda: mul_cyclic(dA, dB, n, out=dC, check=False, err_flag=flag),
+                    reps, warmup, flush)
+    if int(flag.item()) != 0:
+        raise RuntimeError(f"top-bit check fired on seeded inputs (n={n})")
+    t = (n + 63) // 64
+    v = batch / (ms / 1e3)
+    p = eng_plan("cyclic", batch, n)
+    out = {"workload": f"ring mul mod X^{n}-1 x{batch} ({label})", "n": n, "batch": batch,
+           "ms_per_call": round(ms, 4), "value": round(v, 1), "unit": UNIT,
+           "whole_call_frac_int_alu": round(v * w_alg(t) / peak["ops_per_s"], 4),
+           "plan": {"toom_levels": p["toom_levels"], "toom_M": p["toom_M"], "leaf_words": p["leaf_words"],
+                    "levels": p["levels"], "global_levels": p["global_levels"],
+                    "eval_levels": p["eval_levels"], "launches": p["launches"]},
+           "parity": check_rows(np, "cyclic", n, A, B, dC, parity_rows(batch))}
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+    return out
+
+
+def dsweep_entry(torch, np, dev, d, peak, flush, reps=5, warmup=3) -> dict:
+    """configs[4]: unreduced full product of degree-<d operands, batch sized
+    to ~1 GB of operands (A + B) per GPU."""
+    from paper_2201_10473_b200.engine import _WS_BUDGET, _row_chunks, mul_full, plan as eng_plan
+    from paper_2201_10473_b200 import _lib
+
+    t = d // 64
+    batch = DSWEEP_OPERAND_BYTES // (2 * 8 * t)
+    dA = device_words(torch, batch, t, 0xF2F2 + 2 * d, dev)
+    dB = device_words(torch, batch, t, 0xF2F2 + 2 * d + 1, dev)
+    dC = torch.empty((batch, 2 * t), dtype=torch.int64, device=dev)
+    ms = time_calls(torch, lambda: mul_full(dA, dB, out=dC), reps, warmup, flush)
+    v = batch / (ms / 1e3)
+    p = eng_plan("full", batch, t)
+    rows = parity_rows(batch)
+    idx = torch.tensor(rows, dtype=torch.int64, device=dev)
+    hA = np.zeros((batch, t), dtype=np.uint64)  # only the checked rows are filled
+    hB = np.zeros((batch, t), dtype=np.uint64)
+    hA[rows] = dA[idx].cpu().numpy().view(np.uint64)
+    hB[rows] = dB[idx].cpu().numpy().view(np.uint64)
+    chunks = _row_chunks(_lib.load(), _lib.KIND_FULL, batch, t, 0)[0]
+    out = {"workload": f"full product d={d} bits x{batch} (configs[4])", "d": d, "t": t, "batch": batch,
+           "operand_bytes": int(2 * batch * t * 8), "ms_per_call": round(ms, 4), "value": round(v, 1),
+           "unit": UNIT, "whole_call_frac_int_alu": round(v * w_alg(t, cyclic=False) / peak["ops_per_s"], 4),
+           "plan": {"toom_levels": p["toom_levels"], "leaf_words": p["leaf_words"], "levels": p["levels"],
+                    "global_levels": p["global_levels"], "eval_levels": p["eval_levels"],
+                    "workspace_bytes": p["workspace_bytes"], "row_chunks": len(chunks),
+                    "ws_budget": _WS_BUDGET},
+           "parity": check_rows(np, "full", d, hA, hB, dC, rows)}
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+    return out
+
+
+def scaling_block(torch, np, dev, sync, peak, flush, reps=5, warmup=3) -> dict:
+    """configs[3]: n=57637 x 16384 products split 16384/N across the ranks
+    (strong scaling, no data exchange).  Rank 0 also times the whole batch
+    alone (the N=1 point) when N > 1.  Returns rank 0's block."""
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200.engine import mul_cyclic
+
+    n, total = SCALE_N, SCALE_BATCH
+    t = (n + 63) // 64
+    rank, world = sync.rank, sync.world
+    A_all, B_all = make_cyclic_inputs(n, total)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def timed(sl):
+        A, B = np.ascontiguousarray(A_all[sl]), np.ascontiguousarray(B_all[sl])
+        dA = torch.from_numpy(A.view(np.int64)).to(dev)
+        dB = torch.from_numpy(B.view(np.int64)).to(dev)
+        dC = torch.empty_like(dA)
+        ms = time_calls(torch, lambda: mul_cyclic(dA, dB, n, out=dC, check=False, err_flag=flag),
+                        reps, warmup, flush)
+        par = check_rows(np, "cyclic", n, A, B, dC, parity_rows(A.shape[0]))
+        del dA, dB, dC
+        torch.cuda.empty_cache()
+        return ms, par
+
+    solo_ms = None
+    if world > 1:
+        sync.barrier()
+        if rank == 0:
+            solo_ms, _ = timed(slice(0, total))
+        sync.barrier()
+    sl = split_rows(rank, world, total)
+    sync.barrier()
+    ms, par = timed(sl)
+    rows = sl.stop - sl.start
+    per = [0.0] * (3 * world)  # per-rank [ms, rows, ok] gathered through max
+    per[3 * rank], per[3 * rank + 1], per[3 * rank + 2] = ms, rows, 1.0 if par["ok"] else 0.0
+    per = sync.max(per)
+    ok_all = all(per[3 * r + 2] == 1.0 for r in range(world))
+    min_ok = min(per[3 * r + 2] for r in range(world))
+    mx = max(per[3 * r] for r in range(world))
+    if rank != 0:
+        return {}
+    value = total / (mx / 1e3)
+    one = solo_ms if solo_ms is not None else ms
+    W = w_alg(t)
+    return {
+        "workload": f"ring mul mod X^{n}-1, {total} products split {total}/{world} per GPU (configs[3])",
+        "n_gpus": world, "scaling": "strong", "value": round(value, 1), "unit": UNIT,
+        "ms_per_call_max_over_gpus": round(mx, 4),
+        "single_gpu_ms_whole_batch": round(one, 4),
+        "efficiency": round((total / (mx / 1e3)) / (world * total / (one / 1e3)), 4),
+        "per_gpu": [{"device": r, "rows": int(per[3 * r + 1]), "ms_per_call": round(per[3 * r], 4),
+                     "value": round(per[3 * r + 1] / (per[3 * r] / 1e3), 1),
+                     "whole_call_frac_int_alu": round(per[3 * r + 1] / (per[3 * r] / 1e3) * W / peak["ops_per_s"], 4)}
+                    for r in range(world)],
+        "parity": {"rows_checked_per_gpu": par["rows_checked"], "ok": bool(ok_all and min_ok == 1.0)},
+    }
+
+
+def gpu_arm(args, sync, local) -> None:
     import numpy as np
     import torch
 
-    rank, world, local = dist_env()
+    rank, world = sync.rank, sync.world
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
 
     from oracle.f2x_oracle import make_cyclic_inputs
     from paper_2201_10473_b200 import _lib
-    from paper_2201_10473_b200.engine import mul_cyclic, plan
+    from paper_2201_10473_b200.engine import HostPipeline, mul_cyclic, plan
 
     lib = _lib.load()
     n, bpg = args.n, args.batch
     t = (n + 63) // 64
     # one seeded global batch; this rank's contiguous shard
     A_all, B_all = make_cyclic_inputs(n, bpg * world)
-    A = A_all[shard_rows(rank, world, bpg)]
-    B = B_all[shard_rows(rank, world, bpg)]
-    dA = torch.from_numpy(np.ascontiguousarray(A).view(np.int64)).to(dev)
-    dB = torch.from_numpy(np.ascontiguousarray(B).view(np.int64)).to(dev)
+    A = np.ascontiguousarray(A_all[shard_rows(rank, world, bpg)])
+    B = np.ascontiguousarray(B_all[shard_rows(rank, world, bpg)])
+    del A_all, B_all
+    dA = torch.from_numpy(A.view(np.int64)).to(dev)
+    dB = torch.from_numpy(B.view(np.int64)).to(dev)
     dC = torch.empty_like(dA)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -301,9 +569,8 @@ def gpu_arm(args) -> None:
     for a, b in nev:  # torch creates the cudaEvent_t lazily, on first record
         a.record()
         b.record()
-    if world > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize()
+    sync.barrier()
     with ClockSampler(local) as clk:
         for i in range(K):
             flush.fill_(i)
@@ -313,32 +580,21 @@ def gpu_arm(args) -> None:
             ev[i][1].record()
         lib.f2x_set_node_events(None, None)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    sync.barrier()
     step_ms = sum(a.elapsed_time(b) for a, b in ev)
     node_ms = sum(a.elapsed_time(b) for a, b in nev)
     if int(flag.item()) != 0:
         raise RuntimeError("top-bit check fired on seeded inputs")
-
-    # parity spot check of the timed output against the C oracle (not timed)
-    from oracle import c_mul_cyclic
-
-    sub = slice(0, bpg, max(1, bpg // 64))
-    assert np.array_equal(dC.cpu().numpy().view(np.uint64)[sub], c_mul_cyclic(A[sub], B[sub], n)), \
-        "timed output differs from the oracle"
+    head_par = check_rows(np, "cyclic", n, A, B, dC, parity_rows(bpg))
 
     # ---- e2e: host pinned buffers, H2D + compute + D2H inside the timed region
-    from paper_2201_10473_b200.engine import HostPipeline
-
     # several host batches in flight (one pinned buffer set and pipeline lane
     # each) so batch j's H2D/D2H run under batch j-1's kernels; measured on
     # the box (n=17669 x 4096): 1 chunk x 4 lanes 10.6 M/s, 2 x 2 9.7 M/s,
     # 1 x 2 8.5 M/s (a whole-batch launch keeps the node grid at 23 waves)
     LANES = max(1, args.e2e_lanes)
-    hAs = [torch.from_numpy(np.ascontiguousarray(A).view(np.int64).copy()).pin_memory()
-           for _ in range(LANES)]
-    hBs = [torch.from_numpy(np.ascontiguousarray(B).view(np.int64).copy()).pin_memory()
-           for _ in range(LANES)]
+    hAs = [torch.from_numpy(A.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
+    hBs = [torch.from_numpy(B.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
     hCs = [torch.empty_like(hAs[0]).pin_memory() for _ in range(LANES)]
     pipe = HostPipeline("cyclic", n, bpg, dev, chunks=args.e2e_chunks, streams=3, leaf=args.leaf,
                         lanes=LANES)
@@ -355,6 +611,7 @@ def gpu_arm(args) -> None:
         e2e_step()
     pipe.join()
     torch.cuda.synchronize()
+    sync.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     KE = max(3, K // 2)
     e0.record()
@@ -363,24 +620,46 @@ def gpu_arm(args) -> None:
     pipe.join()
     e1.record()
     torch.cuda.synchronize()
+    sync.barrier()
     e2e_ms = e0.elapsed_time(e1) / KE
     if pipe.rejected():
         raise RuntimeError("top-bit check fired on seeded inputs (e2e)")
-    for hC in hCs:
-        assert np.array_equal(hC.numpy().view(np.uint64)[sub], c_mul_cyclic(A[sub], B[sub], n)), \
-            "e2e output differs from the oracle"
+    e2e_ok = True
+    rows = parity_rows(bpg)
+    from oracle import c_mul_cyclic
 
-    # max over ranks
-    stats = torch.tensor([step_ms, node_ms, e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(stats, op=torch.distributed.ReduceOp.MAX)
-    step_ms, node_ms, e2e_ms = stats.tolist()
+    want = c_mul_cyclic(A[rows], B[rows], n)
+    for hC in hCs:
+        e2e_ok &= bool(np.array_equal(hC.numpy().view(np.uint64)[rows], want))
+    del pipe, hAs, hBs, hCs
+
+    # max over ranks (timings), min over ranks (parity) via max of the negation
+    step_ms, node_ms, e2e_ms, bad_head, bad_e2e = sync.max(
+        [step_ms, node_ms, e2e_ms, 0.0 if head_par["ok"] else 1.0, 0.0 if e2e_ok else 1.0])
+    head_par["ok"] = bad_head == 0.0
+    head_par["rows_checked_per_gpu"] = head_par.pop("rows_checked")
     ms_per_step = step_ms / K
     value = bpg * world / (ms_per_step / 1e3)
 
+    scaling = {}
+    if not args.quick:
+        scaling = scaling_block(torch, np, dev, sync, peak, flush)
     per_cfg = {}
     if rank == 0 and world == 1 and not args.quick:
-        per_cfg = extra_configs(torch, np, dev, args, peak)
+        for rn, rb, label in RING_CONFIGS:
+            if rn == SCALE_N and rb == SCALE_BATCH and scaling:
+                continue  # = the scaling block's N=1 point
+            per_cfg[f"n{rn}"] = ring_entry(torch, np, dev, rn, rb, label, peak, flush)
+        if scaling:
+            s1 = scaling["per_gpu"][0]
+            per_cfg[f"n{SCALE_N}"] = {
+                "workload": f"ring mul mod X^{SCALE_N}-1 x{SCALE_BATCH} (configs[3])", "n": SCALE_N,
+                "batch": SCALE_BATCH, "ms_per_call": s1["ms_per_call"], "value": s1["value"], "unit": UNIT,
+                "whole_call_frac_int_alu": s1["whole_call_frac_int_alu"], "parity": scaling["parity"],
+                "note": "same measurement as scaling_57637 at N=1"}
+        if not args.no_dsweep:
+            for d in DSWEEP:
+                per_cfg[f"d{d}"] = dsweep_entry(torch, np, dev, d, peak, flush)
 
     if rank == 0:
         W = w_alg(t)
@@ -389,6 +668,8 @@ def gpu_arm(args) -> None:
         pk = peak["ops_per_s"] / 1e12
         cl = clk.summary()
         nominal = peak["sms"] * 64 * (cl["sm_max_mhz"] or 1965) * 1e6 / 1e12
+        all_ok = head_par["ok"] and e2e_ok and all(e["parity"]["ok"] for e in per_cfg.values()) and \
+            (not scaling or scaling["parity"]["ok"])
         line = {
             "metric": METRIC,
             "value": round(value, 1),
@@ -405,11 +686,14 @@ def gpu_arm(args) -> None:
             "config": {
                 "workload": f"hqc-128 ring mul mod X^{n}-1, {bpg} products/GPU/step (configs[1])",
                 "n": n, "t_words": t, "batch_per_gpu": bpg, "global_batch": bpg * world,
-                "parallelism": f"independent batch shards x{world}, no collectives",
+                "parallelism": f"independent batch shards x{world}; host barrier + max-over-ranks "
+                               f"timing only ({type(sync).__name__}), no NCCL, no collectives",
                 "l2": "flushed before each timed step (256 MiB write, outside events)",
                 "plan": {k: pl[k] for k in ("N", "leaf_words", "levels", "cta_levels",
-                                             "global_levels", "pass_levels", "node_ctas")},
+                                             "global_levels", "pass_levels", "eval_levels", "node_ctas")},
             },
+            "parity": head_par,
+            "parity_all_ok": bool(all_ok),
             "roofline": {
                 "bound": "int_alu",
                 "kernel": "k2_node_mul",
@@ -436,6 +720,7 @@ def gpu_arm(args) -> None:
                 "h2d_bytes_per_step": int(2 * bpg * t * 8),
                 "d2h_bytes_per_step": int(bpg * t * 8),
                 "ms_per_step": round(e2e_ms, 5),
+                "parity_ok": bool(bad_e2e == 0.0),
                 "path": f"pinned host A,B -> H2D -> mul_cyclic (C ABI) -> D2H; engine.HostPipeline, "
                         f"{args.e2e_chunks} row chunk(s) per batch"
                         + (", each batch replayed as one CUDA graph" if graphed else ", eager launches")
@@ -453,56 +738,42 @@ def gpu_arm(args) -> None:
             "gpu_launches": int(K * pl["launches"]),
             "clocks": cl,
         }
+        if scaling:
+            line["scaling_57637"] = scaling
         if per_cfg:
             line["per_config"] = per_cfg
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_reference(n)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+        if not all_ok:
+            print("bench: PARITY FAILURE (see parity fields)", file=sys.stderr)
 
 
-def extra_configs(torch, np, dev, args, peak) -> dict:
-    """n=35851 x4096 and n=57637 x16384 (the metric's other sizes), device timing."""
-    from oracle.f2x_oracle import make_cyclic_inputs
-    from paper_2201_10473_b200.engine import mul_cyclic
+def _spawned_worker(target, rank, world, barrier, arr, targs):
+    target(SpawnSync(rank, world, barrier, arr), rank, *targs)
 
-    out = {}
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    for n, batch in EXTRA_CONFIGS:
-        A, B = make_cyclic_inputs(n, batch)
-        dA = torch.from_numpy(A.view(np.int64)).to(dev)
-        dB = torch.from_numpy(B.view(np.int64)).to(dev)
-        dC = torch.empty_like(dA)
-        for _ in range(3):
-            mul_cyclic(dA, dB, n, out=dC, check=False, err_flag=flag)
-        torch.cuda.synchronize()
-        reps = 5
-        tot = 0.0
-        for i in range(reps):
-            flush.fill_(i)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            mul_cyclic(dA, dB, n, out=dC, check=False, err_flag=flag)
-            e1.record()
-            torch.cuda.synchronize()
-            tot += e0.elapsed_time(e1)
-            if os.environ.get("F2X_BENCH_DEBUG"):
-                print(f"extra n={n} rep {i}: {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
-        ms = tot / reps
-        t = (n + 63) // 64
-        v = batch / (ms / 1e3)
-        from paper_2201_10473_b200.engine import plan as eng_plan
 
-        p = eng_plan("cyclic", batch, n)
-        out[f"n{n}"] = {"batch": batch, "ms_per_call": round(ms, 4), "value": round(v, 1),
-                        "whole_call_frac_int_alu": round(v * w_alg(t) / peak["ops_per_s"], 4),
-                        "plan": {"toom_levels": p["toom_levels"], "toom_M": p["toom_M"],
-                                 "leaf_words": p["leaf_words"], "levels": p["levels"],
-                                 "global_levels": p["global_levels"]}}
-        del dA, dB, dC
-    return out
+def launch_spawned(world: int, target, *targs, timeout_s: float = 1800.0) -> list:
+    """Run target(sync, rank, *targs) in `world` spawned processes (rank r
+    drives cuda:r in the bench) joined by a SpawnSync; returns the exit
+    codes.  A rank that dies breaks the barrier (timeout) instead of hanging
+    the others forever."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    barrier = ctx.Barrier(world, timeout=timeout_s)
+    arr = ctx.Array("d", SpawnSync.SLOTS * world, lock=False)
+    procs = [ctx.Process(target=_spawned_worker, args=(target, r, world, barrier, arr, targs))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join()
+    return [p.exitcode for p in procs]
+
+
+def _gpu_rank(sync, rank, args):
+    gpu_arm(args, sync, rank)
 
 
 def reference_arm(args) -> None:
@@ -559,15 +830,31 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
     ap.add_argument("--e2e-lanes", type=int, default=4,
                     help="host batches in flight in the e2e pipeline (one pinned buffer set each)")
-    ap.add_argument("--quick", action="store_true", help="skip the extra-config lines")
+    ap.add_argument("--quick", action="store_true", help="headline only (no per-config / scaling lines)")
+    ap.add_argument("--no-dsweep", action="store_true", help="skip the configs[4] d-sweep lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "engine":
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+        return
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ:  # torchrun: one process per GPU
+        if world != args.gpus:
+            print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+        sync = GlooSync(rank, world) if world > 1 else LocalSync()
+        try:
+            gpu_arm(args, sync, local)
+        finally:
+            sync.close()
+    elif args.gpus > 1:  # spawn one worker per GPU here
+        codes = launch_spawned(args.gpus, _gpu_rank, args)
+        bad = [c for c in codes if c != 0]
+        if bad:
+            raise SystemExit(f"bench: worker(s) failed with exit codes {bad}")
     else:
-        gpu_arm(args)
+        gpu_arm(args, LocalSync(), 0)
 
 
 if __name__ == "__main__":

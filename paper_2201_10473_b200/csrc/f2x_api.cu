@@ -1193,6 +1193,11 @@ static int debug_sync(cudaStream_t s, int stage) {
 struct DeviceGuard {
     int prev = -1;
     int to_stream(cudaStream_t s) {
+        // (not while the stream is being captured into a graph: the query
+        // would invalidate the capture; a captured call replays on the
+        // graph's device anyway)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
         int sdev = -1, cdev = -1;
         if (cudaStreamGetDevice(s, &sdev) != cudaSuccess || cudaGetDevice(&cdev) != cudaSuccess) return 0;
         if (sdev == cdev) return 0;

@@ -262,8 +262,9 @@ class HostPipeline:
         try:
             with torch.cuda.graph(g):
                 self._enqueue(L, hA, hB, hC)
-        except Exception:
+        except Exception as e:  # noqa: BLE001 -- reported through capture_error
             L["graph"] = None
+            self.capture_error = f"{type(e).__name__}: {e}"
             return False
         L["graph"], L["key"] = g, (hA.data_ptr(), hB.data_ptr(), hC.data_ptr())
         return True

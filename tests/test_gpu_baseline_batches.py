@@ -1,0 +1,146 @@
+"""GPU parity at EXACTLY the BASELINE.json batches (the sizes bench.py
+reports), through the C ABI, against the C oracle:
+
+* configs[0] n=12323 x 256: every row;
+* configs[1] n=17669 x 4096, configs[2] n=35851 x 4096, configs[3]
+  n=57637 x 16384: a 256-row subsample (bench.parity_rows: the first and last
+  32-row groups + an even stride) plus commutativity over the WHOLE batch;
+* configs[4] d-sweep, 1024..65536 bits at ~1 GB of operands per size (the
+  8 GiB workspace budget row-chunks d=65536): subsample + commutativity;
+* very large single products (t = 16384 .. 131072 words) with few rows --
+  the Toom interpolation's sequential fallback for few products -- against
+  the oracle (t=16384) and through bilinearity / commutativity beyond.
+Bit-exact everywhere (integer path, no tolerance)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(x, cuda):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64).view(np.int64)).to(cuda)
+
+
+def _np(x):
+    return x.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("n,batch", [(12323, 256), (17669, 4096), (35851, 4096), (57637, 16384)])
+def test_ring_config_exact_batch(n, batch, cuda):
+    import torch
+
+    import bench
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import mul_cyclic
+
+    A, B = make_cyclic_inputs(n, batch)
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    C = mul_cyclic(dA, dB, n)
+    rows = bench.parity_rows(batch)
+    got = _np(C)[rows]
+    assert np.array_equal(got, c_mul_cyclic(A[rows], B[rows], n))
+    assert torch.equal(C, mul_cyclic(dB, dA, n))
+    if batch <= 256:
+        assert len(rows) == batch
+
+
+@pytest.mark.parametrize("d", [1024, 4096, 8192, 16384, 32768, 65536])
+def test_dsweep_exact_batch(d, cuda):
+    import torch
+
+    import bench
+    from oracle import c_mul_full
+    from paper_2201_10473_b200 import mul_full
+
+    t = d // 64
+    batch = bench.DSWEEP_OPERAND_BYTES // (2 * 8 * t)
+    dA = bench.device_words(torch, batch, t, 0xF2F2 + 2 * d, cuda)
+    dB = bench.device_words(torch, batch, t, 0xF2F2 + 2 * d + 1, cuda)
+    C = mul_full(dA, dB)
+    rows = bench.parity_rows(batch)
+    idx = torch.tensor(rows, device=cuda)
+    A, B = _np(dA[idx]), _np(dB[idx])
+    assert np.array_equal(_np(C[idx]), c_mul_full(A, B))
+    assert torch.equal(C, mul_full(dB, dA))
+
+
+@pytest.mark.parametrize("t,batch", [(16384, 2), (16384, 40)])
+def test_very_large_full_vs_oracle(t, batch, cuda):
+    from oracle import c_mul_full
+    from oracle.f2x_oracle import make_full_inputs
+    from paper_2201_10473_b200 import mul_full
+
+    A, B = make_full_inputs(t, batch, words=True)
+    out = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+    rows = list(range(min(batch, 2)))
+    assert np.array_equal(out[rows], c_mul_full(A[rows], B[rows]))
+
+
+@pytest.mark.parametrize("t", [32768, 65536, 131072])
+def test_very_large_full_properties(t, cuda):
+    import torch
+
+    from oracle.f2x_oracle import make_full_inputs
+    from paper_2201_10473_b200 import mul_full
+
+    A, B = make_full_inputs(t, 3, words=True)
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    C = mul_full(dA, dB)
+    assert torch.equal(C, mul_full(dB, dA))
+    D = torch.roll(dB, 1, 0)
+    assert torch.equal(mul_full(dA, dB ^ D), C ^ mul_full(dA, D))
+    # X^k shift: A * X^(64 j) = A shifted by j words
+    sh = np.zeros_like(A)
+    sh[:, 7] = 1
+    S = _np(mul_full(dA, _dev(sh, cuda)))
+    want = np.zeros((3, 2 * t), dtype=np.uint64)
+    want[:, 7:7 + t] = A
+    assert np.array_equal(S, want)
+
+
+def test_odd_offset_row_views(cuda):
+    """mul_cyclic(A[1:], B[1:], n) at the odd-t config sizes: 8-byte aligned
+    row views are accepted and exact (the reference takes any row)."""
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200 import mul_cyclic, mul_full
+
+    for n in (12323, 17669, 35851, 57637):
+        A, B = make_cyclic_inputs(n, 41)
+        dA, dB = _dev(A, cuda), _dev(B, cuda)
+        assert dA[1:].data_ptr() % 16 == 8
+        assert np.array_equal(_np(mul_cyclic(dA[1:], dB[1:], n)), c_mul_cyclic(A[1:], B[1:], n))
+    A, B = make_full_inputs(3, 9, words=True)
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    assert np.array_equal(_np(mul_full(dA[1:], dB[1:])), c_mul_full(A[1:], B[1:]))
+    # strided (non-contiguous) views are copied, not rejected
+    A, B = make_full_inputs(8, 10, words=True)
+    dA, dB = _dev(A, cuda), _dev(B, cuda)
+    assert np.array_equal(_np(mul_full(dA[:, :4], dB[:, :4])), c_mul_full(A[:, :4], B[:, :4]))
+
+
+def test_bench_two_gpus_spawned(cuda):
+    """`bench.py --gpus 2` without torchrun: two spawned ranks, no NCCL."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun boxes have one)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NCCL_DEBUG="INFO")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3",
+                        "--quick", "--no-cpu"], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["parity"]["ok"]
+    assert "NCCL" not in r.stdout + r.stderr

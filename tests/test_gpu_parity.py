@@ -290,7 +290,7 @@ def test_host_pipeline_graph_replay(cuda):
     hB = torch.from_numpy(B.view(np.int64).copy()).pin_memory()
     hC = torch.empty_like(hA).pin_memory()
     pipe = HostPipeline("cyclic", n, batch, cuda, chunks=4)
-    assert pipe.capture(hA, hB, hC)
+    assert pipe.capture(hA, hB, hC), getattr(pipe, "capture_error", None)
     A2, B2 = np.roll(A, 3, axis=0), np.roll(B, 5, axis=0)
     hA.copy_(torch.from_numpy(A2.view(np.int64)))
     hB.copy_(torch.from_numpy(B2.view(np.int64)))
