@@ -65,8 +65,6 @@ static inline int64_t ipow5(int k) {
     while (k-- > 0) r *= 5;
     return r;
 }
-// row stride of a plain Toom operand of 3M coefficients: whole 16-byte quads
-static inline int64_t toom_opstride(int64_t M) { return (3 * M + 3) / 4 * 4; }
 static inline int64_t ipow3(int k) {
     int64_t r = 1;
     while (k-- > 0) r *= 3;
@@ -251,102 +249,273 @@ k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, ui
 }
 
 // --------------------------------------------------------------- Toom-3
-// One Toom-3 evaluation level (paper Appendix D): operand
-// item i (3M coefficients, plain bitsliced, stride inS) -> items 5i+e,
-// e = 0, 1, x, x+1, inf with x = X^w, of S >= M + 2w coefficients in the
-// (LFo, LFSo) chunked layout (plain when LFo == LFSo), stride outS.  In the
-// bitsliced layout multiplying by x is an index shift, so each output word is
-// an XOR of at most 5 input words.  Both operands (blockIdx.y).
-__global__ void __launch_bounds__(256)
-toom_eval_level(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
-                uint32_t *__restrict__ Yb, int64_t items_in, int64_t inS, int M, int w, int S, int LFo,
-                int LFSo, int64_t outS) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= items_in * outS) return;
-    const int64_t i = idx / outS;
-    const int sw = int(idx - i * outS);
-    int k;
-    bool valid;
-    if (LFo == LFSo) {
-        k = sw;
-        valid = k < S;
-    } else {
-        const int c = sw / LFSo, r = sw - c * LFSo;
-        k = c * LFo + r;
-        valid = r < LFo && k < S;
-    }
-    const uint32_t *x = (blockIdx.y ? Xb : Xa) + i * inS;
-    uint32_t a0 = 0, a1 = 0, a2 = 0, s1 = 0, s2 = 0;
-    if (valid) {
-        if (k < M) {
-            a0 = __ldg(x + k);
-            a1 = __ldg(x + M + k);
-            a2 = __ldg(x + 2 * M + k);
-        }
-        if (k >= w && k - w < M) s1 = __ldg(x + M + k - w);
-        if (k >= 2 * w && k - 2 * w < M) s2 = __ldg(x + 2 * M + k - 2 * w);
-    }
-    uint32_t *y = (blockIdx.y ? Yb : Ya) + i * 5 * outS + sw;
-    const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
-    y[0] = a0;
-    y[outS] = p1;
-    y[2 * outS] = a0 ^ xs;
-    y[3 * outS] = p1 ^ xs;
-    y[4 * outS] = a2;
+// ---------------------------------------------------------- fused Toom eval
+// All TL Toom-3 evaluation levels in ONE pass (instead of TL launches with
+// HBM round trips of the intermediate levels): a CTA owns one (group,
+// operand, tile of Tc node-problem chunks = T coefficients) and produces that
+// tile of all 5^TL node-problem operands.  Evaluation is local: a
+// level-(l+1) coefficient k reads level-l coefficients k, M+k, 2M+k, M+k-w,
+// 2M+k-2w (M = M_{l+1}), so a level-(l+1) window of length L needs three
+// level-l windows ("pieces") of length L + 2w.  Piece pi at level l has
+// digits (p_{l+1} .. p_TL), most significant first, and starts at
+// sigma_l(pi) = p_{l+1} M_{l+1} + sigma_{l+1}(rest) - 2w (sigma_TL = tile
+// start k0).  The planner makes every M_l, the level-0 row and k0 multiples
+// of 4 coefficients, so every piece is 16-byte aligned in HBM and in shared
+// memory and every mask boundary (k = 0, M, M+w, M+2w) falls on a quad:
+//   * the 3^TL level-0 pieces are staged by bulk async copies
+//     (cp.async.bulk, completion on an mbarrier, no register staging);
+//   * the intermediate levels are built in shared memory depth first, one
+//     16-byte quad (4 coefficients) per thread-item, masks per quad;
+//   * the last level is written as chunked storage quads (16-byte stores).
+struct ToomEvalGeo {
+    int M[4];       // M[1..TL]: part sizes (multiples of 4)
+    int N0;         // level-0 operand coefficients (3 M_1, plain)
+    int LF, LFS;    // node-problem chunk layout
+    int chunks;     // node-problem chunks (2^K)
+    int Tc;         // chunks per tile (Tc LF multiple of 4)
+    int64_t G;      // groups
+    int64_t Ns;     // storage words per node-problem operand
+};
+
+constexpr int kEvalFusedThreads = 256;
+constexpr int kEvalFusedMaxT = 288;  // coefficients per tile (Tc LF <= 288)
+
+__host__ __device__ constexpr int efpow3(int k) { return k <= 0 ? 1 : 3 * efpow3(k - 1); }
+// piece slot words at level l (pieces of T + 2w (TL - l) coefficients)
+__host__ __device__ constexpr int efslot(int TL, int l) { return kEvalFusedMaxT + 2 * kToomW * (TL - l); }
+
+// shared-memory words: L0 (3^TL pieces), then for TL = 3 one e1's L1 (9
+// pieces) and all five e2's L2 (15 pieces), for TL = 2 all five e1's L1
+__host__ __device__ constexpr int eval_fused_smem_words(int TL) {
+    return efpow3(TL) * efslot(TL, 0) +
+           (TL == 3 ? 9 * efslot(3, 1) + 15 * efslot(3, 2) : TL == 2 ? 15 * efslot(2, 1) : 0);
 }
 
-// Quad form of toom_eval_level (outS and LFSo multiples of 4, 16-byte
-// aligned outputs): grid (output quads / 256, input items, operand), one
-// output storage QUAD per thread -- no 64-bit index division, one chunk
-// split per quad (a quad never straddles a chunk), 16-byte stores.  The
-// per-word form was issue-bound (72-78 % issue slots at n=57637).
-__global__ void __launch_bounds__(256)
-toom_eval_level_q(const uint32_t *__restrict__ Xa, const uint32_t *__restrict__ Xb, uint32_t *__restrict__ Ya,
-                  uint32_t *__restrict__ Yb, int64_t inS, int M, int w, int S, int LFo, int LFSo, int64_t outS) {
-    const int sq = int(blockIdx.x) * 256 + int(threadIdx.x);
-    const int sw0 = 4 * sq;
-    if (sw0 >= outS) return;
-    const int64_t i = blockIdx.y;
-    int k0, r0, lim;
-    if (LFo == LFSo) {
-        k0 = sw0;
-        r0 = 0;
-        lim = 4;
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+
+// Evaluation of quad jq (coefficients 4jq..4jq+3 of the next-level piece,
+// first coordinate k) from the three level-l pieces: E = -1 all five points,
+// else only point E (0, 1, x, x+1, inf).  Quads at local j+2w, j+w, j.
+template <int E>
+__device__ __forceinline__ void eval_quad(const uint4 *P0, const uint4 *P1, const uint4 *P2, int jq, int k, int M,
+                                          uint4 (&y)[E < 0 ? 5 : 1]) {
+    constexpr int wq = kToomW / 4;
+    const bool ka = unsigned(k) < unsigned(M), k1 = unsigned(k - kToomW) < unsigned(M),
+               k2 = unsigned(k - 2 * kToomW) < unsigned(M);
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    const bool use_a0 = E < 0 || E <= 3, use_a1 = E < 0 || E == 1 || E == 3,
+               use_a2 = E < 0 || E == 1 || E == 3 || E == 4, use_s = E < 0 || E == 2 || E == 3;
+    const uint4 a0 = (use_a0 && ka) ? P0[jq + 2 * wq] : z;
+    const uint4 a1 = (use_a1 && ka) ? P1[jq + 2 * wq] : z;
+    const uint4 a2 = (use_a2 && ka) ? P2[jq + 2 * wq] : z;
+    const uint4 s1 = (use_s && k1) ? P1[jq + wq] : z;
+    const uint4 s2 = (use_s && k2) ? P2[jq] : z;
+    if constexpr (E < 0) {
+        const uint4 p1 = xor3(a0, a1, a2), xs = s1 ^ s2;
+        y[0] = a0;
+        y[1] = p1;
+        y[2] = a0 ^ xs;
+        y[3] = p1 ^ xs;
+        y[4] = a2;
+    } else if constexpr (E == 0) {
+        y[0] = a0;
+    } else if constexpr (E == 1) {
+        y[0] = xor3(a0, a1, a2);
+    } else if constexpr (E == 2) {
+        y[0] = xor3(a0, s1, s2);
+    } else if constexpr (E == 3) {
+        y[0] = xor3(a0, a1, a2) ^ (s1 ^ s2);
     } else {
-        const int c = sw0 / LFSo;
-        r0 = sw0 - c * LFSo;
-        k0 = c * LFo + r0;
-        lim = LFo - r0;  // words r < lim of the quad hold data
+        y[0] = a2;
     }
-    const uint32_t *x = (blockIdx.z ? Xb : Xa) + i * inS;
-    uint32_t y0[4], y1[4], y2[4], y3[4], y4[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int k = k0 + r;
-        uint32_t a0 = 0, a1 = 0, a2 = 0, s1 = 0, s2 = 0;
-        if (r < lim && k < S) {
-            if (k < M) {
-                a0 = __ldg(x + k);
-                a1 = __ldg(x + M + k);
-                a2 = __ldg(x + 2 * M + k);
-            }
-            if (k >= w && k - w < M) s1 = __ldg(x + M + k - w);
-            if (k >= 2 * w && k - 2 * w < M) s2 = __ldg(x + 2 * M + k - 2 * w);
+}
+
+// level-1 pieces (9 of them) of one evaluation point E from the 27 level-0
+// pieces (TL = 3)
+template <int E>
+__device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo, int k0,
+                                              int nq1, int tid) {
+    constexpr int w = kToomW, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
+    for (int pi1 = 0; pi1 < 9; ++pi1) {
+        const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
+        const int sig1 = p2 * geo.M[2] + p3 * geo.M[3] + k0 - 4 * w;
+        const uint4 *P0 = reinterpret_cast<const uint4 *>(L0 + pi1 * Z0);
+        const uint4 *P1 = reinterpret_cast<const uint4 *>(L0 + (9 + pi1) * Z0);
+        const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
+        uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
+        for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
+            uint4 y[1];
+            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, geo.M[1], y);
+            D[jq] = y[0];
         }
-        const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
-        y0[r] = a0;
-        y1[r] = p1;
-        y2[r] = a0 ^ xs;
-        y3[r] = p1 ^ xs;
-        y4[r] = a2;
     }
-    uint4 *y = reinterpret_cast<uint4 *>((blockIdx.z ? Yb : Ya) + i * 5 * outS + sw0);
-    const int64_t o4 = outS / 4;
-    y[0] = make_uint4(y0[0], y0[1], y0[2], y0[3]);
-    y[o4] = make_uint4(y1[0], y1[1], y1[2], y1[3]);
-    y[2 * o4] = make_uint4(y2[0], y2[1], y2[2], y2[3]);
-    y[3 * o4] = make_uint4(y3[0], y3[1], y3[2], y3[3]);
-    y[4 * o4] = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+}
+
+// all five points of nq quads of `np` pieces at once: piece p of the output
+// (of every point e) from input pieces (0, p), (1, p), (2, p) (stride np);
+// output piece (e, p) at D + (e np + p) Zd
+__device__ __forceinline__ void eval_level5(const uint32_t *S, int Zs, uint32_t *D, int Zd, int np, int nq,
+                                            const int *sig, int M, int tid) {
+    for (int p = 0; p < np; ++p) {
+        const uint4 *P0 = reinterpret_cast<const uint4 *>(S + p * Zs);
+        const uint4 *P1 = reinterpret_cast<const uint4 *>(S + (np + p) * Zs);
+        const uint4 *P2 = reinterpret_cast<const uint4 *>(S + (2 * np + p) * Zs);
+        for (int jq = tid; jq < nq; jq += kEvalFusedThreads) {
+            uint4 y[5];
+            eval_quad<-1>(P0, P1, P2, jq, sig[p] + 4 * jq, M, y);
+#pragma unroll
+            for (int e = 0; e < 5; ++e) reinterpret_cast<uint4 *>(D + (e * np + p) * Zd)[jq] = y[e];
+        }
+    }
+}
+
+template <int TL>
+__global__ void __launch_bounds__(kEvalFusedThreads, 3)
+toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint32_t *__restrict__ Yb,
+                const ToomEvalGeo geo, int64_t x0_words) {
+    constexpr int w = kToomW;
+    constexpr int NP0 = efpow3(TL), Z0 = efslot(TL, 0);
+    extern __shared__ __align__(16) uint32_t efs[];
+    __shared__ __align__(8) uint64_t mbar;
+    const int tid = threadIdx.x;
+    const int tiles = (geo.chunks + geo.Tc - 1) / geo.Tc;
+    const int64_t g = blockIdx.x / tiles;
+    const int tile = int(blockIdx.x - g * tiles);
+    const int op = blockIdx.y;
+    const int LF = geo.LF, LFS = geo.LFS;
+    const int c0 = tile * geo.Tc;
+    const int tc = min(geo.Tc, geo.chunks - c0);  // chunks in this tile
+    const int T = (tc * LF + 3) & ~3;             // coefficients (whole quads)
+    const int k0 = c0 * LF;                       // multiple of 4 (planner)
+    uint32_t *L0 = efs;
+
+    // ---- stage the level-0 pieces: one bulk copy per piece (lanes of warp 0)
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t bytes = 0, dst = 0;
+        int64_t src = 0;
+        if (tid < NP0) {
+            int sig = k0, rem = tid;  // sigma_0 of piece tid, digits p_TL first
+#pragma unroll
+            for (int l = TL; l >= 1; --l) {
+                const int p = rem % 3;
+                rem /= 3;
+                sig = p * geo.M[l] + sig - 2 * w;
+            }
+            const int64_t A = (int64_t(op) * geo.G + g) * geo.N0 + sig;  // 16-byte aligned word index
+            const int64_t E = A + T + 2 * w * TL;
+            const int64_t a0c = A < 0 ? 0 : A, ec = E > x0_words ? x0_words : E;
+            if (ec > a0c) {  // (words outside the operand are never read unmasked)
+                bytes = uint32_t(ec - a0c) * 4u;
+                src = a0c;
+                dst = smem_u32(L0 + tid * Z0 + (a0c - A));
+            }
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)),
+                         "r"(total)
+                         : "memory");
+        __syncwarp();
+        if (bytes)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                "l"(X0 + src), "r"(bytes), "r"(smem_u32(&mbar))
+                : "memory");
+    }
+    // per-thread final-level work, fixed for the CTA: storage quad qi of the
+    // tile (chunk c, words r0..r0+3) for items e_last = tid / nq (+ 256 / nq ..)
+    const int nq = (tc * LFS) >> 2;
+    {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(smem_u32(&mbar))
+                : "memory");
+    }
+    uint32_t *out = (op ? Yb : Ya) + int64_t(c0) * LFS;
+    const int Mt = geo.M[TL];
+    // interior tile: every mask of the last level is true (no per-word checks)
+    const bool interior = k0 >= 2 * w && k0 + tc * LF <= Mt;
+    // final level: the 5 points of storage quad qi from the three pieces of
+    // the level-(TL-1) window (item5 -> items 5 item5 + e)
+    auto final_quad = [&](const uint32_t *P0, const uint32_t *P1, const uint32_t *P2, int64_t item5, int qi) {
+        const int s0 = qi * 4;
+        const int c = s0 / LFS, r0 = s0 - c * LFS;
+        uint32_t v[5][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int j = c * LF + r0 + r, k = k0 + j;
+            const bool data = r0 + r < LF;
+            const bool ka = data && (interior || unsigned(k) < unsigned(Mt));
+            const bool k1 = data && (interior || unsigned(k - w) < unsigned(Mt));
+            const bool k2 = data && (interior || unsigned(k - 2 * w) < unsigned(Mt));
+            const uint32_t a0 = ka ? P0[j + 2 * w] : 0u, a1 = ka ? P1[j + 2 * w] : 0u, a2 = ka ? P2[j + 2 * w] : 0u;
+            const uint32_t s1 = k1 ? P1[j + w] : 0u, s2 = k2 ? P2[j] : 0u;
+            const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
+            v[0][r] = a0;
+            v[1][r] = p1;
+            v[2][r] = a0 ^ xs;
+            v[3][r] = p1 ^ xs;
+            v[4][r] = a2;
+        }
+#pragma unroll
+        for (int e = 0; e < 5; ++e)
+            *reinterpret_cast<uint4 *>(out + (item5 * 5 + e) * geo.Ns + s0) =
+                make_uint4(v[e][0], v[e][1], v[e][2], v[e][3]);
+    };
+    if constexpr (TL == 1) {
+        for (int qi = tid; qi < nq; qi += kEvalFusedThreads) final_quad(L0, L0 + Z0, L0 + 2 * Z0, g, qi);
+    } else if constexpr (TL == 2) {
+        constexpr int Z1 = efslot(2, 1);
+        uint32_t *L1 = L0 + NP0 * Z0;  // [e1][p2]
+        int sig[3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) sig[p] = p * geo.M[2] + k0 - 2 * w;
+        eval_level5(L0, Z0, L1, Z1, 3, (T + 2 * w) >> 2, sig, geo.M[1], tid);
+        __syncthreads();
+        for (int it = tid; it < 5 * nq; it += kEvalFusedThreads) {
+            const int e1 = it / nq, qi = it - e1 * nq;
+            const uint32_t *P = L1 + e1 * 3 * Z1;
+            final_quad(P, P + Z1, P + 2 * Z1, g * 5 + e1, qi);
+        }
+    } else {
+        static_assert(TL == 3, "1..3 Toom levels");
+        constexpr int Z1 = efslot(3, 1), Z2 = efslot(3, 2);
+        uint32_t *L1 = L0 + NP0 * Z0;  // [p2 p3] (9 pieces) of one e1
+        uint32_t *L2 = L1 + 9 * Z1;    // [e2][p3] (15 pieces)
+        const int nq1 = (T + 4 * w) >> 2, nq2 = (T + 2 * w) >> 2;
+        int sig2[3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
+#pragma unroll 1
+        for (int e1 = 0; e1 < 5; ++e1) {
+            switch (e1) {
+                case 0: eval_l1_point<0>(L0, L1, geo, k0, nq1, tid); break;
+                case 1: eval_l1_point<1>(L0, L1, geo, k0, nq1, tid); break;
+                case 2: eval_l1_point<2>(L0, L1, geo, k0, nq1, tid); break;
+                case 3: eval_l1_point<3>(L0, L1, geo, k0, nq1, tid); break;
+                default: eval_l1_point<4>(L0, L1, geo, k0, nq1, tid); break;
+            }
+            __syncthreads();
+            eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, geo.M[2], tid);
+            __syncthreads();
+            for (int it = tid; it < 5 * nq; it += kEvalFusedThreads) {
+                const int e2 = it / nq, qi = it - e2 * nq;
+                const uint32_t *P = L2 + e2 * 3 * Z2;
+                final_quad(P, P + Z2, P + 2 * Z2, (g * 5 + e1) * 5 + e2, qi);
+            }
+            // (the next level-1 pass writes only L1; L2 is rewritten after its barrier)
+        }
+    }
 }
 
 // One Toom-3 interpolation level, from the 5 products C_e of every output
@@ -887,7 +1056,7 @@ struct Layout {
     int tl = 0;                      // Toom-3 levels
     int64_t G2 = 0;                  // node-problem groups (G 5^tl)
     int64_t M[kMaxToom + 1] = {};    // Toom part sizes, level 1..tl
-    int64_t off_x[kMaxToom] = {};    // Toom operands: [0] plain slice, [l] level-l outputs
+    int64_t off_x0 = 0;              // Toom plans: plain bitsliced slice (both operands)
     int64_t off_r[kMaxToom + 1] = {};  // Toom interpolation outputs, level l
     int64_t off_q[kMaxToom + 1] = {};  // level-l c_0..c_4 before carries (5 x 2M per item)
     int64_t off_tot[kMaxToom + 1] = {};  // level-l chain totals per block
@@ -946,8 +1115,10 @@ static bool best_leaf(int64_t Smin, int leaf_hint, int &bestLF, int &bestK, doub
 // S_l >= M_l + 2w coefficients; S_l = 3 M_{l+1} below another Toom level,
 // the node size LF 2^K at the last.  Sizes for Nmin coefficients:
 static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
-    M[1] = ceil_div(Nmin, 3);
-    for (int l = 1; l < TL; ++l) M[l + 1] = ceil_div(M[l] + 2 * kToomW, 3);
+    // multiples of 4 coefficients: every Toom piece is a whole 16-byte quad
+    // (toom_eval_fused); costs <= 3 coefficients of padding per level
+    M[1] = (ceil_div(Nmin, 3) + 3) & ~int64_t(3);
+    for (int l = 1; l < TL; ++l) M[l + 1] = (ceil_div(M[l] + 2 * kToomW, 3) + 3) & ~int64_t(3);
     Smin_last = M[TL] + 2 * kToomW;
 }
 
@@ -991,6 +1162,16 @@ static int toom_override() {
     return v;
 }
 
+// F2X_TOOM_LEAF=LF forces the node-problem leaf of Toom plans (experiments;
+// a leaf_hint argument forces the leaf AND disables Toom)
+static int toom_leaf_override() {
+    static const int v = [] {
+        const char *e = getenv("F2X_TOOM_LEAF");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
                      Layout *lay) {
     if (!pl || batch < 1 || t_or_n < 1) return F2X_EINVAL;
@@ -1019,7 +1200,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
         int LF, K;
         double c;
-        if (!best_leaf(Smin, leaf_hint, LF, K, c)) continue;
+        if (!best_leaf(Smin, TL > 0 && toom_leaf_override() ? toom_leaf_override() : leaf_hint, LF, K, c)) continue;
         c *= double(ipow5(TL));
         // Toom passes are HBM-bound: ~kToomWordCost per word moved per group
         for (int l = 1; l <= TL; ++l) {
@@ -1089,13 +1270,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.Ss = int64_t(LFS) << KC;
     L.el = TL ? 0 : eval_levels_for(GL, int64_t(LF) << K);
     int64_t off = 0;
-    if (TL > 0) {  // plain bitsliced operand and the upper Toom levels' operands
-        L.off_x[0] = off;
+    if (TL > 0) {  // plain bitsliced operands (the fused evaluation's input)
+        L.off_x0 = off;
         off = align256(off + 2 * G * 3 * L.M[1] * 4);
-        for (int l = 1; l < TL; ++l) {
-            L.off_x[l] = off;
-            off = align256(off + 2 * G * ipow5(l) * toom_opstride(L.M[l + 1]) * 4);
-        }
     }
     const int64_t opw = G2 * ipow3(L.el) * (L.Ns >> L.el);  // node-problem operand words
     L.off_abs = off;
@@ -1243,45 +1420,45 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     if (L.tl > 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
-        uint32_t *X0a = reinterpret_cast<uint32_t *>(w + L.off_x[0]);
+        uint32_t *X0a = reinterpret_cast<uint32_t *>(w + L.off_x0);
         F2X_LAUNCH(k1_slice, grid, kTileThreads, 0, stream, A, B, X0a, X0a + G * int64_t(pl.N), batch, pl.t, pl.N,
                                                     pl.N, pl.N, int64_t(pl.N), ncyc, d_err, tiles);
         if ((rc = debug_sync(stream, 1))) return rc;
-        // Toom evaluation levels: level l < tl writes plain operands of
-        // 3 M_{l+1} coefficients, the last one the node problem's chunked
-        // operands (LF 2^K coefficients)
-        for (int l = 1; l <= L.tl; ++l) {
-            const uint32_t *xa = reinterpret_cast<const uint32_t *>(w + L.off_x[l - 1]);
-            const int64_t items_in = G * ipow5(l - 1), inS = l == 1 ? 3 * L.M[1] : toom_opstride(L.M[l]);
-            const uint32_t *xb = xa + items_in * inS;
-            uint32_t *ya, *yb;
-            int S, LFo, LFSo;
-            int64_t outS;
-            if (l < L.tl) {
-                ya = reinterpret_cast<uint32_t *>(w + L.off_x[l]);
-                S = int(3 * L.M[l + 1]);
-                LFo = LFSo = S;
-                outS = toom_opstride(L.M[l + 1]);  // whole quads; pad words written 0
-                yb = ya + items_in * 5 * outS;
-            } else {
-                ya = Abs;
-                yb = Bbs;
-                S = pl.leaf_words << pl.levels;
-                LFo = pl.leaf_words;
-                LFSo = pl.leaf_stride;
-                outS = L.Ns;
-            }
-            if (outS % 4 == 0 && (LFo == LFSo || LFSo % 4 == 0) && items_in <= 65535) {
-                dim3 grid(unsigned(ceil_div(outS / 4, 256)), unsigned(items_in), 2);
-                F2X_LAUNCH(toom_eval_level_q, grid, 256, 0, stream, xa, xb, ya, yb, inS, int(L.M[l]), kToomW, S, LFo,
-                                                            LFSo, outS);
-            } else {
-                dim3 grid(unsigned(ceil_div(items_in * outS, 256)), 2);
-                F2X_LAUNCH(toom_eval_level, grid, 256, 0, stream, xa, xb, ya, yb, items_in, inS, int(L.M[l]), kToomW,
-                                                          S, LFo, LFSo, outS);
-            }
-            if ((rc = debug_sync(stream, 1))) return rc;
+        ToomEvalGeo geo{};
+        for (int l = 1; l <= L.tl; ++l) geo.M[l] = int(L.M[l]);
+        geo.N0 = pl.N;
+        geo.LF = pl.leaf_words;
+        geo.LFS = pl.leaf_stride;
+        geo.chunks = 1 << pl.levels;
+        // Tc LF must be a multiple of 4 (quad-aligned tiles)
+        geo.Tc = 8 * pl.leaf_words <= kEvalFusedMaxT ? 8 : 4;
+        geo.G = G;
+        geo.Ns = L.Ns;
+        const int etiles = int(ceil_div(geo.chunks, geo.Tc));
+        const size_t sm = size_t(eval_fused_smem_words(L.tl)) * 4;
+        static std::atomic<uint32_t> ef_dev_mask{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 31 && !(ef_dev_mask.load() & (1u << dev))) {
+            cudaError_t ae = cudaFuncSetAttribute(toom_eval_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(eval_fused_smem_words(1) * 4));
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_eval_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(eval_fused_smem_words(2) * 4));
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_eval_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(eval_fused_smem_words(3) * 4));
+            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
+            ef_dev_mask.fetch_or(1u << dev);
         }
+        const dim3 egrid(unsigned(etiles * G), 2);
+        const int64_t x0w = 2 * G * int64_t(pl.N);
+        switch (L.tl) {
+            case 1: F2X_LAUNCH(toom_eval_fused<1>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
+            case 2: F2X_LAUNCH(toom_eval_fused<2>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
+            default: F2X_LAUNCH(toom_eval_fused<3>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
+        }
+        if ((rc = debug_sync(stream, 2))) return rc;
     } else if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);

@@ -8,6 +8,7 @@ from oracle.f2x_oracle import make_cyclic_inputs
 from paper_2201_10473_b200 import mul_cyclic
 
 dev = torch.device("cuda", 0)
+leaf = int(os.environ.get("LEAF", "0"))
 for arg in sys.argv[1:] or ["17669"]:
     n, batch = (int(x) for x in (arg.split(":") + ["4096"])[:2])
     A, B = make_cyclic_inputs(n, min(batch, 4096))
@@ -16,12 +17,12 @@ for arg in sys.argv[1:] or ["17669"]:
     dB = torch.from_numpy(np.tile(B, (reps, 1)).view(np.int64)).to(dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     for _ in range(3):
-        mul_cyclic(dA, dB, n, check=False, err_flag=flag)
+        mul_cyclic(dA, dB, n, check=False, err_flag=flag, leaf=leaf)
     torch.cuda.synchronize()
     R = 10
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(R):
-            mul_cyclic(dA, dB, n, check=False, err_flag=flag)
+            mul_cyclic(dA, dB, n, check=False, err_flag=flag, leaf=leaf)
         torch.cuda.synchronize()
     tot = {}
     for e in prof.events():
