@@ -12,6 +12,13 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "libf2x.so")
+# F2X_LIB_VARIANT=leaky|checked loads a TEST FIXTURE built from the same
+# sources (build.py VARIANTS) instead: used only by the constant-time
+# positive control and the shared-memory initcheck tests, each in its own
+# process
+_VARIANT = os.environ.get("F2X_LIB_VARIANT")
+if _VARIANT in ("leaky", "checked"):
+    LIB_PATH = os.path.join(HERE, f"_build_{_VARIANT}", f"libf2x_{_VARIANT}.so")
 
 F2X_OK = 0
 F2X_EINVAL = -22

@@ -121,6 +121,8 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
          uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns,
          int ncyc, uint32_t *d_err, int tiles) {
     __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
+    check_poison(stage, sizeof(stage));
+    check_poison_sync();
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
     const int tile = int(blockIdx.x - g * tiles);
@@ -153,6 +155,16 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     // store the contiguous storage range of coefficients [k0, k1)
     const int k0 = tile * kTileCoeffs, k1 = min(k0 + kTileCoeffs, N);
     if (k0 >= k1) return;
+    if (LF == LFS && (Ns & 3) == 0 && (k1 & 3) == 0) {
+        // plain layout (Toom plans' slice): storage = coefficients, whole
+        // 16-byte quads (the tile starts on a quad; N and Ns are quads)
+        uint4 *o = reinterpret_cast<uint4 *>(out + k0);
+        for (int q = tid; q < ((k1 - k0) >> 2); q += kTileThreads) {
+            const int k = 4 * q;
+            o[q] = make_uint4(stage[stg(k)], stage[stg(k + 1)], stage[stg(k + 2)], stage[stg(k + 3)]);
+        }
+        return;
+    }
     int c, r;
     chunk_split(k0, LF, c, r);
     const int s0 = c * LFS + r;
@@ -172,79 +184,88 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
 // writes the 3^EL evaluated sub-operands (per level: lo, hi, lo^hi; top level
 // most significant -- the node numbering of the node kernel is unchanged; it
 // runs on 3^EL x the groups with K-EL levels and loads 2^EL x fewer segments
-// per mid path).
+// per mid path).  A tile is TW operand words of each part covering WHOLE
+// chunks (64 TW a multiple of LF: TW = LF, or the whole part), so its storage
+// range is a run of whole 16-byte quads: the second phase writes storage
+// quads (one 16-byte store per sub-operand and quad) and no two CTAs share a
+// quad.  Thread x < 2^EL 2 TW owns half-word column x of the tile (one 32x32
+// bit transpose); all threads walk the quads.
 template <int EL>
-__global__ void __launch_bounds__(kTileThreads << EL)
+__global__ void __launch_bounds__(512)
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
               int ncyc, uint32_t *d_err, int tiles, int TW) {
-    // TW (<= 64) operand words per tile: the part is cut into `tiles`
-    // balanced tiles, so no CTA carries a nearly empty tail tile
     constexpr int NP = 1 << EL;               // parts
     constexpr int NO = EL == 1 ? 3 : 9;       // evaluated sub-operands
     const int STG = 64 * TW + 2 * TW;         // stage words per part (1 pad per 32)
     extern __shared__ uint32_t stage[];       // [NP][STG]
-    const int tid = threadIdx.x & (kTileThreads - 1);
-    const int j = threadIdx.x / kTileThreads;  // part handled by this thread's 128-group
+    check_poison(stage, unsigned(NP * STG * 4));
+    check_poison_sync();
+    const int x = threadIdx.x, nthr = blockDim.x;
     const int64_t g = blockIdx.x / tiles;
     const int tile = int(blockIdx.x - g * tiles);
     const int NE = N >> EL;                   // coefficients per part (multiple of 64)
     const uint32_t *X = reinterpret_cast<const uint32_t *>(blockIdx.y ? B : A);
-    uint32_t *out = (blockIdx.y ? Eb : Ea) + g * (NO * NsE);
     const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
-    const int half = tid & 1;
-    const int ul = tile * TW + (tid >> 1);  // word within the part
-    if (tid < 2 * TW) {
-        const int u = j * (NE / 64) + ul;  // operand word
-        uint32_t x[32];
+    if (x < NP * 2 * TW) {
+        const int j = x / (2 * TW), h = x - j * (2 * TW);  // part, half-word column in the tile
+        const int half = h & 1;
+        const int ul = tile * TW + (h >> 1);  // word within the part
+        const int u = j * (NE / 64) + ul;     // operand word
+        uint32_t xv[32];
         uint32_t bad = 0;
         const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
                                     ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
                                     : 0u;
-        const int r = (u < t && ul < NE / 64) ? rows : 0;
+        const int r = u < t ? rows : 0;
         const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
 #pragma unroll
         for (int pr = 0; pr < 32; ++pr) {
             const uint32_t v = pr < r ? __ldg(px) : 0u;
             px += 2 * int64_t(t);
             bad |= v & himask;
-            x[pr] = v;
+            xv[pr] = v;
         }
         if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
             atomicOr(d_err, uint32_t(bad != 0));
-        transpose32(x);
+        transpose32(xv);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) stage[j * STG + stg(32 * tid + i)] = x[i];
+        for (int i = 0; i < 32; ++i) stage[j * STG + stg(32 * h + i)] = xv[i];
     }
     __syncthreads();
-    const int k0 = tile * 64 * TW, k1 = min(k0 + 64 * TW, NE);
-    if (k0 >= k1) return;
-    int c, r;
-    chunk_split(k0, LF, c, r);
-    const int s0 = c * LFS + r;
-    chunk_split(k1, LF, c, r);
-    const int s1 = c * LFS + r;
-    // all NP x 128 threads walk the storage range (stride NP x 128)
-    StorageWalkN<(kTileThreads << EL)> w(s0 + int(threadIdx.x), k0, LF, LFS);
-#pragma unroll 2
-    for (int sw = s0 + int(threadIdx.x); sw < s1; sw += kTileThreads << EL) {
-        uint32_t v[NP];
+    const int nc = (64 * TW) / LF;  // whole chunks per tile
+    const int qpc = LFS >> 2, nq = nc * qpc;
+    uint32_t *out = (blockIdx.y ? Eb : Ea) + g * (NO * NsE) + int64_t(tile) * nc * LFS;
+    for (int q = x; q < nq; q += nthr) {
+        const int c = q / qpc, r0 = (q - c * qpc) * 4;
+        const int kb = c * LF + r0;  // tile-local coefficient of the quad's first word
+        uint32_t v[NP][4];
 #pragma unroll
-        for (int jj = 0; jj < NP; ++jj) v[jj] = w.data() ? stage[jj * STG + stg(w.kk)] : 0u;
+        for (int rr = 0; rr < 4; ++rr) {
+            const bool data = r0 + rr < LF;
+#pragma unroll
+            for (int jj = 0; jj < NP; ++jj) v[jj][rr] = data ? stage[jj * STG + stg(kb + rr)] : 0u;
+        }
+        uint4 *o = reinterpret_cast<uint4 *>(out) + q;
+        const int64_t s4 = NsE >> 2;  // sub-operand stride in quads
         if constexpr (EL == 1) {
-            out[sw] = v[0];
-            out[NsE + sw] = v[1];
-            out[2 * NsE + sw] = v[0] ^ v[1];
+            const uint4 lo = make_uint4(v[0][0], v[0][1], v[0][2], v[0][3]);
+            const uint4 hi = make_uint4(v[1][0], v[1][1], v[1][2], v[1][3]);
+            o[0] = lo;
+            o[s4] = hi;
+            o[2 * s4] = lo ^ hi;
         } else {
-            const uint32_t h[3][2] = {{v[0], v[1]}, {v[2], v[3]}, {v[0] ^ v[2], v[1] ^ v[3]}};
+            uint4 p[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) p[jj] = make_uint4(v[jj][0], v[jj][1], v[jj][2], v[jj][3]);
+            const uint4 h[3][2] = {{p[0], p[1]}, {p[2], p[3]}, {p[0] ^ p[2], p[1] ^ p[3]}};
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                out[(3 * d) * NsE + sw] = h[d][0];
-                out[(3 * d + 1) * NsE + sw] = h[d][1];
-                out[(3 * d + 2) * NsE + sw] = h[d][0] ^ h[d][1];
+                o[(3 * d) * s4] = h[d][0];
+                o[(3 * d + 1) * s4] = h[d][1];
+                o[(3 * d + 2) * s4] = h[d][0] ^ h[d][1];
             }
         }
-        w.next();
     }
 }
 
@@ -332,12 +353,16 @@ __device__ __forceinline__ void eval_quad(const uint4 *P0, const uint4 *P1, cons
     }
 }
 
-// level-1 pieces (9 of them) of one evaluation point E from the 27 level-0
-// pieces (TL = 3)
-template <int E>
+// level-1 pieces (9 of them) of one evaluation point e (0, 1, x, x+1, inf;
+// uniform, runtime: predicated loads -- no per-point code copies) from the 27
+// level-0 pieces (TL = 3)
 __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo, int k0,
-                                              int nq1, int tid) {
-    constexpr int w = kToomW, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
+                                              int nq1, int tid, int e) {
+    constexpr int w = kToomW, wq = kToomW / 4, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
+    const bool use_a0 = e != 4, use_a1 = e == 1 || e == 3, use_a2 = e == 1 || e == 3 || e == 4,
+               use_s = e == 2 || e == 3;
+    const int M = geo.M[1];
+    const uint4 z = make_uint4(0, 0, 0, 0);
     for (int pi1 = 0; pi1 < 9; ++pi1) {
         const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
         const int sig1 = p2 * geo.M[2] + p3 * geo.M[3] + k0 - 4 * w;
@@ -346,9 +371,15 @@ __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, 
         const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
         uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
         for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
-            uint4 y[1];
-            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, geo.M[1], y);
-            D[jq] = y[0];
+            const int k = sig1 + 4 * jq;
+            const bool ka = unsigned(k) < unsigned(M), k1 = unsigned(k - w) < unsigned(M),
+                       k2 = unsigned(k - 2 * w) < unsigned(M);
+            const uint4 a0 = (use_a0 && ka) ? P0[jq + 2 * wq] : z;
+            const uint4 a1 = (use_a1 && ka) ? P1[jq + 2 * wq] : z;
+            const uint4 a2 = (use_a2 && ka) ? P2[jq + 2 * wq] : z;
+            const uint4 s1 = (use_s && k1) ? P1[jq + wq] : z;
+            const uint4 s2 = (use_s && k2) ? P2[jq] : z;
+            D[jq] = xor3(a0, a1, a2) ^ (s1 ^ s2);
         }
     }
 }
@@ -379,6 +410,8 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
     constexpr int NP0 = efpow3(TL), Z0 = efslot(TL, 0);
     extern __shared__ __align__(16) uint32_t efs[];
     __shared__ __align__(8) uint64_t mbar;
+    check_poison(efs, unsigned(eval_fused_smem_words(TL) * 4));
+    check_poison_sync();
     const int tid = threadIdx.x;
     const int tiles = (geo.chunks + geo.Tc - 1) / geo.Tc;
     const int64_t g = blockIdx.x / tiles;
@@ -498,13 +531,7 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
         for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
 #pragma unroll 1
         for (int e1 = 0; e1 < 5; ++e1) {
-            switch (e1) {
-                case 0: eval_l1_point<0>(L0, L1, geo, k0, nq1, tid); break;
-                case 1: eval_l1_point<1>(L0, L1, geo, k0, nq1, tid); break;
-                case 2: eval_l1_point<2>(L0, L1, geo, k0, nq1, tid); break;
-                case 3: eval_l1_point<3>(L0, L1, geo, k0, nq1, tid); break;
-                default: eval_l1_point<4>(L0, L1, geo, k0, nq1, tid); break;
-            }
+            eval_l1_point(L0, L1, geo, k0, nq1, tid, e1);
             __syncthreads();
             eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, geo.M[2], tid);
             __syncthreads();
@@ -568,6 +595,8 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     const int H = kToomBlk + 3 * w;          // staged span per input
     constexpr int HP = kToomStgStride;        // padded stride per input (see tstg)
     uint32_t *Stg = tsm;                      // [5][H], index k - (k0 - 2w)
+    check_poison(tsm, unsigned(5 * HP * 4));
+    check_poison_sync();
     const int64_t item = blockIdx.x / nb;
     const int b = int(blockIdx.x - item * nb);
     const int L = 2 * M, k0 = b * kToomBlk, kb = k0 - 2 * w;
@@ -611,6 +640,8 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     // through shared memory
     constexpr int W = kToomW, ROWS = kToomBlk / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
     __shared__ uint32_t stot[3][NSEG][W];
+    check_poison(stot, sizeof(stot));
+    check_poison_sync();
     const int r = int(threadIdx.x) % W, sg = int(threadIdx.x) / W;
     const int kr = k0 + sg * SEGR * W + r;  // first coefficient of this thread
     uint32_t v1[SEGR], v2[SEGR], v3[SEGR];
@@ -682,6 +713,10 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
     uint32_t *Stg = tsm;  // [5][HP]
     __shared__ uint32_t stot[3][NSEG][W];
     __shared__ uint32_t bcar[3][W];  // carry into the current block, per chain
+    check_poison(tsm, unsigned(5 * HP * 4));
+    check_poison(stot, sizeof(stot));
+    check_poison(bcar, sizeof(bcar));
+    check_poison_sync();
     const int64_t item = blockIdx.x;
     const int L = 2 * M, nb = (L + BLK - 1) / BLK;
     const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
@@ -754,7 +789,12 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
 #pragma unroll
             for (int e = 0; e < 5; ++e) {
 #pragma unroll
-                for (int i = 0; i < NI; ++i) v[e][i] = ok[i] ? __ldg(Ce + off[i]) : 0u;
+                for (int i = 0; i < NI; ++i) {
+                    // unconditional load from a clamped in-row offset, value masked:
+                    // no predicated address arithmetic (tools/ct_sass_audit.py)
+                    const uint32_t x = __ldg(Ce + (ok[i] ? off[i] : 0));
+                    v[e][i] = ok[i] ? x : 0u;
+                }
                 Ce += inS;
             }
             __syncthreads();  // previous block's readers of Stg / stot are done
@@ -860,6 +900,8 @@ __global__ void __launch_bounds__(256)
 toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict__ Tot, uint32_t *__restrict__ R,
                      int M, int w, int nb, int nbo, int64_t outS) {
     extern __shared__ uint32_t carry[];  // [nb][3][w]
+    check_poison(carry, unsigned(nb * 3 * w * 4));
+    check_poison_sync();
     const int64_t item = blockIdx.x / nbo;
     const int ob = int(blockIdx.x - item * nbo);
     const int L = 2 * M;
@@ -994,6 +1036,8 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
     constexpr int TC = 64 * TW, TT = 2 * TW;  // coefficients, threads per tile
     __shared__ uint32_t stage[TC + TC / 32];
+    check_poison(stage, sizeof(stage));
+    check_poison_sync();
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x / tiles;
     const int tile = int(blockIdx.x - g * tiles);
@@ -1002,33 +1046,45 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
     for (int k = k0 + tid; k < k0 + TC; k += TT)
         if (k >= kvalid) stage[stg(k - k0)] = 0u;
-    int c, r;
-    if (k0 < kvalid) {
-        chunk_split(k0, LF, c, r);
+    // gather root coefficients [ka, kb) into stage index k - ka (XOR when
+    // folding) as 16-byte storage quads; words outside the range or in chunk
+    // pads are skipped (root rows are whole quads: the over-fetch at the ends
+    // stays inside the row)
+    auto gather = [&](int ka, int kb, bool fold) {
+        int c, r;
+        chunk_split(ka, LF, c, r);
         const int s0 = c * LFS + r;
-        chunk_split(kvalid, LF, c, r);
+        chunk_split(kb, LF, c, r);
         const int s1 = c * LFS + r;
-        StorageWalkN<TT> w(s0 + tid, k0, LF, LFS);
-#pragma unroll 8
-        for (int sw = s0 + tid; sw < s1; sw += TT) {
-            const uint32_t v = __ldg(Cg + sw);  // pads too: loads batch across the unroll
-            if (w.data()) stage[stg(w.kk)] = v;
-            w.next();
+        const uint4 *C4 = reinterpret_cast<const uint4 *>(Cg);
+        const int qa = (s0 >> 2) + tid, qb = (s1 + 3) >> 2;
+        // every load of the range in flight at once (one L2/HBM round trip):
+        // <= KQ quads per thread (tile of 64 TW coefficients, <= 1.25 storage
+        // words per coefficient)
+        constexpr int KQ = (64 * TW * 5 / 4 / 4 + TT - 1) / TT + 1;
+        uint4 v[KQ];
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) v[i] = qa + i * TT < qb ? __ldg(C4 + qa + i * TT) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) {
+            const int q = qa + i * TT;
+            if (q >= qb) break;
+            const uint32_t vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            const int sw = 4 * q, cq = sw / LFS, rq = sw - cq * LFS;
+            const int kq = cq * LF + rq - ka;
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                if (sw + rr >= s0 && sw + rr < s1 && rq + rr < LF) {
+                    if (fold) stage[stg(kq + rr)] ^= vv[rr];
+                    else stage[stg(kq + rr)] = vv[rr];
+                }
+            }
         }
-    }
+    };
+    if (k0 < kvalid) gather(k0, kvalid, false);
     __syncthreads();
     if (ncyc > 0 && k0 < kvalid) {  // fold: coefficients [k0+n, kvalid+n)
-        chunk_split(k0 + ncyc, LF, c, r);
-        const int s0 = c * LFS + r;
-        chunk_split(kvalid + ncyc, LF, c, r);
-        const int s1 = c * LFS + r;
-        StorageWalkN<TT> w(s0 + tid, k0 + ncyc, LF, LFS);
-#pragma unroll 8
-        for (int sw = s0 + tid; sw < s1; sw += TT) {
-            const uint32_t v = __ldg(Cg + sw);
-            if (w.data()) stage[stg(w.kk)] ^= v;
-            w.next();
-        }
+        gather(k0 + ncyc, kvalid + ncyc, true);
         __syncthreads();
     }
     uint32_t x[32];
@@ -1466,10 +1522,13 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                                                     pl.leaf_words, pl.leaf_stride, L.Ns, ncyc,
                                                     d_err, tiles);
     } else {
-        // balanced tiles of <= 64 words per part
+        // tiles of whole chunks: TW = LF words per part (64 chunks) when the
+        // part holds >= 64 chunks, else the whole part
         const int pw = (pl.N >> L.el) / 64;
-        const int tiles = int(ceil_div(pw, kTileWords));
-        const int TW = int(ceil_div(pw, tiles));
+        const int levels_left = pl.levels - L.el;
+        const int TW = levels_left >= 6 ? pl.leaf_words : pw;
+        const int tiles = pw / TW;
+        const int nthr = int(ceil_div((1 << L.el) * 2 * TW, 32) * 32);
         dim3 grid(unsigned(G * tiles), 2);
         const size_t sm = size_t(1 << L.el) * (64 * TW + 2 * TW) * 4;
         const size_t sm_max = size_t(1 << L.el) * (64 * kTileWords + 2 * kTileWords) * 4;
@@ -1484,11 +1543,11 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             attr_dev_mask[L.el].fetch_or(1u << dev);
         }
         if (L.el == 1) {
-            F2X_LAUNCH(k1_slice_eval<1>, grid, kTileThreads << 1, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
+            F2X_LAUNCH(k1_slice_eval<1>, grid, nthr, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
                                                                  L.Ns >> 1, ncyc, d_err, tiles, TW);
         } else {
-            F2X_LAUNCH(k1_slice_eval<2>, grid, kTileThreads << 2, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
+            F2X_LAUNCH(k1_slice_eval<2>, grid, nthr, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
                                                                  pl.leaf_words, pl.leaf_stride,
                                                                  L.Ns >> 2, ncyc, d_err, tiles, TW);
         }

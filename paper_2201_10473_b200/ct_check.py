@@ -2,11 +2,16 @@
 
 Fixed-vs-random timing test: a weight-w sparse first operand (the HQC secret
 shape) against a dense random first operand, interleaved
-trials, Welch's t statistic on the per-call times; |t| < 4.5 passes.  On the
-GPU every call is timed with CUDA events around one ring product of a batch
-of 32 (one bitsliced group).  ``leaky_mul`` is the positive control the SPEC
-asks for: a sparse convolution that only visits the set bits of A (its time
-grows with the weight), which must fail.
+trials, Welch's t statistic on the per-call times; |t| < 4.5 passes; fewer
+than 10^4 trials ("pre: trials >= 10^4") is "inconclusive".  On
+the GPU every call is timed with CUDA events around one ring product of a
+batch of 32 (one bitsliced group).  Controls:
+
+* ``control=True``: dense fixed vs dense random -- must pass;
+* the deliberately leaky GPU build (``F2X_LIB_VARIANT=leaky``, the
+  ``F2X_LEAKY_LEAF`` fixture: leaves skip all-zero a words) -- must FAIL;
+* ``leaky_mul``: a CPU sparse convolution that only visits the set bits of
+  A -- must FAIL (``ct_check_leaky``).
 """
 
 from __future__ import annotations
@@ -17,6 +22,7 @@ import time
 import numpy as np
 
 THRESHOLD = 4.5
+MIN_TRIALS = 10_000
 
 
 def welch_t(x, y) -> float:
@@ -44,9 +50,11 @@ def _dense_rows(n: int, rows: int, rng) -> np.ndarray:
     return A
 
 
-def ct_check(n: int = 17669, weight: int = 75, trials: int = 2000, seed: int = 0xC7,
-             batch: int = 32) -> dict:
-    """GPU fixed(sparse)-vs-random(dense) timing test of ``mul_cyclic``."""
+def ct_check(n: int = 17669, weight: int = 75, trials: int = MIN_TRIALS, seed: int = 0xC7,
+             batch: int = 32, control: bool = False) -> dict:
+    """GPU fixed-vs-random(dense) timing test of ``mul_cyclic``: the fixed
+    first operand is weight-``weight`` sparse, or dense with ``control``.
+    ``trials`` calls per class."""
     import torch
 
     from .engine import mul_cyclic
@@ -54,7 +62,8 @@ def ct_check(n: int = 17669, weight: int = 75, trials: int = 2000, seed: int = 0
     rng = np.random.default_rng(seed)
     dev = torch.device("cuda", torch.cuda.current_device())
     B = torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev)
-    sparse = torch.from_numpy(_sparse_rows(n, weight, batch, rng).view(np.int64)).to(dev)
+    fixed = _dense_rows(n, batch, rng) if control else _sparse_rows(n, weight, batch, rng)
+    sparse = torch.from_numpy(fixed.view(np.int64)).to(dev)
     pool = [torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev) for _ in range(8)]
     out = torch.empty_like(B)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -63,7 +72,7 @@ def ct_check(n: int = 17669, weight: int = 75, trials: int = 2000, seed: int = 0
     torch.cuda.synchronize()
     t_fix, t_rnd = [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    order = rng.integers(0, 2, size=2 * trials)
+    order = rng.permutation(np.repeat([0, 1], trials))  # exactly `trials` per class, interleaved
     for i, cls in enumerate(order):
         A = sparse if cls == 0 else pool[i % len(pool)]
         e0.record()
@@ -72,9 +81,12 @@ def ct_check(n: int = 17669, weight: int = 75, trials: int = 2000, seed: int = 0
         e1.synchronize()
         (t_fix if cls == 0 else t_rnd).append(e0.elapsed_time(e1))
     t = welch_t(t_fix, t_rnd)
-    return {"n": n, "weight": weight, "trials": [len(t_fix), len(t_rnd)],
-            "mean_ms": [float(np.mean(t_fix)), float(np.mean(t_rnd))], "t": t,
-            "verdict": "pass" if abs(t) < THRESHOLD else "fail"}
+    verdict = "pass" if abs(t) < THRESHOLD else "fail"
+    if min(len(t_fix), len(t_rnd)) < MIN_TRIALS and verdict == "pass":
+        verdict = "inconclusive"  # too few trials to call it constant time
+    return {"n": n, "weight": None if control else weight, "control": control,
+            "trials": [len(t_fix), len(t_rnd)],
+            "mean_ms": [float(np.mean(t_fix)), float(np.mean(t_rnd))], "t": t, "verdict": verdict}
 
 
 def leaky_mul(a: int, b: int, n: int) -> int:
@@ -106,6 +118,11 @@ def ct_check_leaky(n: int = 2000, weight: int = 20, trials: int = 300, seed: int
 
 if __name__ == "__main__":
     import json
+    import sys
 
-    print(json.dumps(ct_check()))
-    print(json.dumps(ct_check_leaky()))
+    if "--control" in sys.argv:
+        print(json.dumps(ct_check(control=True)))
+    else:
+        print(json.dumps(ct_check()))
+    if "--cpu-leaky" in sys.argv:
+        print(json.dumps(ct_check_leaky()))

@@ -33,9 +33,66 @@ def test_leaky_mul_is_correct():
 
 @pytest.mark.gpu
 def test_gpu_ring_mul_constant_time(cuda):
+    """Weight-75 sparse vs dense at hqc-128, 10^4 calls per class."""
     from paper_2201_10473_b200.ct_check import ct_check
 
-    r = ct_check(n=17669, weight=75, trials=1500)
+    r = ct_check(n=17669, weight=75, trials=10_000)
     if r["verdict"] != "pass":  # flaky-tolerant: one retry (SPEC.md:487)
-        r = ct_check(n=17669, weight=75, trials=1500, seed=0xC9)
+        r = ct_check(n=17669, weight=75, trials=10_000, seed=0xC9)
     assert r["verdict"] == "pass", r
+
+
+@pytest.mark.gpu
+def test_gpu_dense_vs_dense_control_passes(cuda):
+    """dense fixed vs dense random (identical distributions)."""
+    from paper_2201_10473_b200.ct_check import ct_check
+
+    r = ct_check(n=17669, trials=10_000, control=True)
+    if r["verdict"] != "pass":
+        r = ct_check(n=17669, trials=10_000, control=True, seed=0xCA)
+    assert r["verdict"] == "pass", r
+
+
+@pytest.mark.gpu
+def test_gpu_leaky_fixture_fails(cuda):
+    """SPEC.md:472 positive control ON THE GPU: the same engine built with
+    F2X_LEAKY_LEAF=1 (leaves skip all-zero a words: a data-dependent branch)
+    still computes the right products but must FAIL the Welch test, proving
+    the test can see a leak of that size."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from paper_2201_10473_b200 import build as b
+
+    if not os.path.exists(b.LIB_LEAKY):
+        pytest.skip("leaky fixture not built (build.build(leaky=True))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import json, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2201_10473_b200 import _lib, mul_cyclic
+from paper_2201_10473_b200.ct_check import ct_check
+from oracle import c_mul_cyclic
+from oracle.f2x_oracle import make_cyclic_inputs
+assert _lib.LIB_PATH.endswith("libf2x_leaky.so"), _lib.LIB_PATH
+A, B = make_cyclic_inputs(17669, 64)
+d = lambda x: torch.from_numpy(x.view(np.int64)).cuda()
+assert np.array_equal(mul_cyclic(d(A), d(B), 17669).cpu().numpy().view(np.uint64), c_mul_cyclic(A, B, 17669))
+print(json.dumps(ct_check(n=17669, weight=75, trials=10_000)))
+"""
+    env = dict(os.environ, F2X_LIB_VARIANT="leaky")
+    r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["verdict"] == "fail", res
+
+
+def test_too_few_trials_is_inconclusive(monkeypatch):
+    """SPEC.md:469 (trials >= 10^4): a passing statistic on fewer trials is
+    not a pass."""
+    from paper_2201_10473_b200 import ct_check as ct
+
+    assert ct.MIN_TRIALS == 10_000
