@@ -353,16 +353,14 @@ __device__ __forceinline__ void eval_quad(const uint4 *P0, const uint4 *P1, cons
     }
 }
 
-// level-1 pieces (9 of them) of one evaluation point e (0, 1, x, x+1, inf;
-// uniform, runtime: predicated loads -- no per-point code copies) from the 27
-// level-0 pieces (TL = 3)
+// level-1 pieces (9 of them) of one evaluation point E from the 27 level-0
+// pieces (TL = 3); E is a compile-time constant (the e1 loop is unrolled:
+// each point reads only the pieces it needs, and there is no indirect branch
+// -- tools/ct_sass_audit.py)
+template <int E>
 __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo, int k0,
-                                              int nq1, int tid, int e) {
-    constexpr int w = kToomW, wq = kToomW / 4, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
-    const bool use_a0 = e != 4, use_a1 = e == 1 || e == 3, use_a2 = e == 1 || e == 3 || e == 4,
-               use_s = e == 2 || e == 3;
-    const int M = geo.M[1];
-    const uint4 z = make_uint4(0, 0, 0, 0);
+                                              int nq1, int tid) {
+    constexpr int w = kToomW, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
     for (int pi1 = 0; pi1 < 9; ++pi1) {
         const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
         const int sig1 = p2 * geo.M[2] + p3 * geo.M[3] + k0 - 4 * w;
@@ -371,15 +369,9 @@ __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, 
         const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
         uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
         for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
-            const int k = sig1 + 4 * jq;
-            const bool ka = unsigned(k) < unsigned(M), k1 = unsigned(k - w) < unsigned(M),
-                       k2 = unsigned(k - 2 * w) < unsigned(M);
-            const uint4 a0 = (use_a0 && ka) ? P0[jq + 2 * wq] : z;
-            const uint4 a1 = (use_a1 && ka) ? P1[jq + 2 * wq] : z;
-            const uint4 a2 = (use_a2 && ka) ? P2[jq + 2 * wq] : z;
-            const uint4 s1 = (use_s && k1) ? P1[jq + wq] : z;
-            const uint4 s2 = (use_s && k2) ? P2[jq] : z;
-            D[jq] = xor3(a0, a1, a2) ^ (s1 ^ s2);
+            uint4 y[1];
+            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, geo.M[1], y);
+            D[jq] = y[0];
         }
     }
 }
@@ -529,9 +521,13 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
         int sig2[3];
 #pragma unroll
         for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
-#pragma unroll 1
+#pragma unroll
         for (int e1 = 0; e1 < 5; ++e1) {
-            eval_l1_point(L0, L1, geo, k0, nq1, tid, e1);
+            if (e1 == 0) eval_l1_point<0>(L0, L1, geo, k0, nq1, tid);
+            if (e1 == 1) eval_l1_point<1>(L0, L1, geo, k0, nq1, tid);
+            if (e1 == 2) eval_l1_point<2>(L0, L1, geo, k0, nq1, tid);
+            if (e1 == 3) eval_l1_point<3>(L0, L1, geo, k0, nq1, tid);
+            if (e1 == 4) eval_l1_point<4>(L0, L1, geo, k0, nq1, tid);
             __syncthreads();
             eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, geo.M[2], tid);
             __syncthreads();

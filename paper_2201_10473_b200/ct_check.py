@@ -4,8 +4,12 @@ Fixed-vs-random timing test: a weight-w sparse first operand (the HQC secret
 shape) against a dense random first operand, interleaved
 trials, Welch's t statistic on the per-call times; |t| < 4.5 passes; fewer
 than 10^4 trials ("pre: trials >= 10^4") is "inconclusive".  On
-the GPU every call is timed with CUDA events around one ring product of a
-batch of 32 (one bitsliced group).  Controls:
+the GPU every call is timed with CUDA events around one ring-product call of
+a batch of 4096 (the configs[1] batch; every row of the fixed class has a
+weight-w first operand).  At batch 32 (one bitsliced group) the call is
+launch-latency bound and even the leaky fixture below passed (measured), so
+the test had no detection power there; at 4096 the leaves dominate.
+Controls (SPEC.md:470-472):
 
 * ``control=True``: dense fixed vs dense random -- must pass;
 * the deliberately leaky GPU build (``F2X_LIB_VARIANT=leaky``, the
@@ -51,7 +55,7 @@ def _dense_rows(n: int, rows: int, rng) -> np.ndarray:
 
 
 def ct_check(n: int = 17669, weight: int = 75, trials: int = MIN_TRIALS, seed: int = 0xC7,
-             batch: int = 32, control: bool = False) -> dict:
+             batch: int = 4096, control: bool = False) -> dict:
     """GPU fixed-vs-random(dense) timing test of ``mul_cyclic``: the fixed
     first operand is weight-``weight`` sparse, or dense with ``control``.
     ``trials`` calls per class."""
@@ -63,18 +67,28 @@ def ct_check(n: int = 17669, weight: int = 75, trials: int = MIN_TRIALS, seed: i
     dev = torch.device("cuda", torch.cuda.current_device())
     B = torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev)
     fixed = _dense_rows(n, batch, rng) if control else _sparse_rows(n, weight, batch, rng)
-    sparse = torch.from_numpy(fixed.view(np.int64)).to(dev)
-    pool = [torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev) for _ in range(8)]
+    # both classes cycle through the same number of distinct device buffers
+    # (the fixed class: 8 copies of the fixed operand) and L2 is flushed
+    # before every call, so the classes differ ONLY in the operand bits --
+    # a single re-used fixed buffer would stay L2-resident and time faster
+    NBUF = 8
+    fixed_bufs = [torch.from_numpy(fixed.view(np.int64).copy()).to(dev) for _ in range(NBUF)]
+    pool = [torch.from_numpy(_dense_rows(n, batch, rng).view(np.int64)).to(dev) for _ in range(NBUF)]
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)  # 256 MiB > L2
     out = torch.empty_like(B)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    for _ in range(10):
-        mul_cyclic(sparse, B, n, out=out, check=False, err_flag=flag)
+    for i in range(10):
+        mul_cyclic(fixed_bufs[i % NBUF], B, n, out=out, check=False, err_flag=flag)
+        mul_cyclic(pool[i % NBUF], B, n, out=out, check=False, err_flag=flag)
     torch.cuda.synchronize()
     t_fix, t_rnd = [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     order = rng.permutation(np.repeat([0, 1], trials))  # exactly `trials` per class, interleaved
-    for i, cls in enumerate(order):
-        A = sparse if cls == 0 else pool[i % len(pool)]
+    seen = [0, 0]
+    for cls in order:
+        A = (fixed_bufs if cls == 0 else pool)[seen[cls] % NBUF]
+        seen[cls] += 1
+        flush.fill_(int(seen[0] + seen[1]))
         e0.record()
         mul_cyclic(A, B, n, out=out, check=False, err_flag=flag)
         e1.record()
