@@ -1002,10 +1002,14 @@ __device__ __forceinline__ void k3_rec(uint32_t *out, const uint32_t *__restrict
     }
 }
 
+// plainLF > 0 (the last pass of a Toom plan): the output root is written
+// PLAIN -- chunk pads dropped, coefficient c LF + r at word c LF + r -- so
+// the Toom interpolation stages it with 16-byte loads; qw is a multiple of
+// LFS there, so all of a thread's words share one chunk residue r.
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t items, int qw,
-          int64_t inStride, int64_t outStride) {
+          int64_t inStride, int64_t outStride, int plainLF, int LFS) {
     // blocks walk the nodes in REVERSE order: the node kernel wrote them in
     // forward order, so the most recently written (still L2-resident)
     // products are consumed first instead of being evicted by the rest
@@ -1016,6 +1020,14 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
     const int w = int(item - node * qw);
     uint32_t v[4 << D];
     k3_rec<D>(v, Pin, inStride, node, qw, w);  // leaves: node*3^D + local
+    if (plainLF > 0) {
+        const int c0 = w / LFS, r = w - c0 * LFS, qc = qw / LFS;
+        if (r >= plainLF) return;  // a chunk pad: not stored in the plain root
+        uint32_t *dst = Pout + node * outStride + int64_t(c0) * plainLF + r;
+#pragma unroll
+        for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qc * plainLF] = v[m];
+        return;
+    }
     uint32_t *dst = Pout + node * outStride + w;
 #pragma unroll
     for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qw] = v[m];
@@ -1367,8 +1379,9 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
 
 template <int D>
 static int launch_k3(const uint32_t *Pin, uint32_t *Pout, int64_t items, int qw, int64_t inS,
-                     int64_t outS, cudaStream_t s) {
-    k3_interp<D><<<unsigned(ceil_div(items, kThreads)), kThreads, 0, s>>>(Pin, Pout, items, qw, inS, outS);
+                     int64_t outS, int plainLF, int LFS, cudaStream_t s) {
+    k3_interp<D><<<unsigned(ceil_div(items, kThreads)), kThreads, 0, s>>>(Pin, Pout, items, qw, inS, outS,
+                                                                          plainLF, LFS);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : F2X_ECUDA - int(e);
 }
@@ -1574,11 +1587,16 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int qw = int(Shi / 2);
         const int64_t items = L.G2 * ipow3(dlo) * qw;
         const int64_t inS = i == 0 ? in_stride0 : 2 * Shi;
+        // the last pass of a Toom plan writes the node-problem root plain
+        // (2 LF 2^K words per root) for the interpolation's 16-byte staging
+        const bool plain_root = L.tl > 0 && i == pl.num_passes - 1 && dlo == 0;
+        const int pLF = plain_root ? pl.leaf_words : 0;
+        const int64_t outS = plain_root ? 2 * (int64_t(pl.leaf_words) << pl.levels) : 2 * Slo;
         switch (D) {
-            case 1: rc = launch_k3<1>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 2: rc = launch_k3<2>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 3: rc = launch_k3<3>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
-            case 4: rc = launch_k3<4>(cur, nxt, items, qw, inS, 2 * Slo, stream); break;
+            case 1: rc = launch_k3<1>(cur, nxt, items, qw, inS, outS, pLF, pl.leaf_stride, stream); break;
+            case 2: rc = launch_k3<2>(cur, nxt, items, qw, inS, outS, pLF, pl.leaf_stride, stream); break;
+            case 3: rc = launch_k3<3>(cur, nxt, items, qw, inS, outS, pLF, pl.leaf_stride, stream); break;
+            case 4: rc = launch_k3<4>(cur, nxt, items, qw, inS, outS, pLF, pl.leaf_stride, stream); break;
             default: return F2X_ERANGE;
         }
         if (rc) return rc;
@@ -1592,6 +1610,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     const uint32_t *root = cur;
     int rootLF = pl.leaf_words, rootLFS = pl.leaf_stride;
     int64_t rootS = pl.num_passes == 0 ? in_stride0 : 2 * L.Ns;
+    if (L.tl > 0 && pl.num_passes > 0) {  // plain root (last K3 pass above)
+        rootS = 2 * (int64_t(pl.leaf_words) << pl.levels);
+        rootLF = rootLFS = int(rootS);
+    }
     for (int l = L.tl; l >= 1; --l) {
         uint32_t *out = reinterpret_cast<uint32_t *>(w + L.off_r[l]);
         uint32_t *Q = reinterpret_cast<uint32_t *>(w + L.off_q[l]);
