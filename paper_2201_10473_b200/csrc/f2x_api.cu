@@ -361,16 +361,18 @@ template <int E>
 __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo, int k0,
                                               int nq1, int tid) {
     constexpr int w = kToomW, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
+    const int M2 = geo.M[2], M3 = geo.M[3], M1 = geo.M[1];
+#pragma unroll
     for (int pi1 = 0; pi1 < 9; ++pi1) {
         const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
-        const int sig1 = p2 * geo.M[2] + p3 * geo.M[3] + k0 - 4 * w;
+        const int sig1 = p2 * M2 + p3 * M3 + k0 - 4 * w;
         const uint4 *P0 = reinterpret_cast<const uint4 *>(L0 + pi1 * Z0);
         const uint4 *P1 = reinterpret_cast<const uint4 *>(L0 + (9 + pi1) * Z0);
         const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
         uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
         for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
             uint4 y[1];
-            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, geo.M[1], y);
+            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, M1, y);
             D[jq] = y[0];
         }
     }
@@ -381,7 +383,8 @@ __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, 
 // output piece (e, p) at D + (e np + p) Zd
 __device__ __forceinline__ void eval_level5(const uint32_t *S, int Zs, uint32_t *D, int Zd, int np, int nq,
                                             const int *sig, int M, int tid) {
-    for (int p = 0; p < np; ++p) {
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
         const uint4 *P0 = reinterpret_cast<const uint4 *>(S + p * Zs);
         const uint4 *P1 = reinterpret_cast<const uint4 *>(S + (np + p) * Zs);
         const uint4 *P2 = reinterpret_cast<const uint4 *>(S + (2 * np + p) * Zs);
@@ -454,9 +457,28 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
                 "l"(X0 + src), "r"(bytes), "r"(smem_u32(&mbar))
                 : "memory");
     }
-    // per-thread final-level work, fixed for the CTA: storage quad qi of the
-    // tile (chunk c, words r0..r0+3) for items e_last = tid / nq (+ 256 / nq ..)
+    // final level, per-thread work fixed for the whole CTA: item slots it =
+    // tid + 256 u < 5 nq -> (point e, storage quad qi of the tile); a quad
+    // holds the consecutive coefficients j0 .. j0+3 of one chunk (data mask
+    // dm: pads are zero); precomputed once, no division in the loops
     const int nq = (tc * LFS) >> 2;
+    // 5 nq <= 2 x 256: nq = Tc LFS / 4 <= 88 (Tc = 8 up to LF = 36, else 4; LFS <= 44)
+    constexpr int FS = 2;
+    int fe[FS], fs0[FS], fj0[FS];
+    uint32_t fdm[FS];
+#pragma unroll
+    for (int u = 0; u < FS; ++u) {
+        const int it = tid + u * kEvalFusedThreads;
+        const int e = it / nq, qi = it - e * nq;
+        const int s0 = qi * 4, c = s0 / LFS, r0 = s0 - c * LFS;
+        fe[u] = it < 5 * nq ? e : -1;
+        fs0[u] = s0;
+        fj0[u] = c * LF + r0;
+        fdm[u] = (LF - r0 >= 4) ? 0xFu : ((1u << max(LF - r0, 0)) - 1u);
+    }
+    const int Mt = geo.M[TL];
+    // interior tile: every mask of the last level is true (no per-word checks)
+    const bool interior = k0 >= 2 * w && k0 + tc * LF <= Mt;
     {
         uint32_t done = 0;
         while (!done)
@@ -467,38 +489,63 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
                 : "memory");
     }
     uint32_t *out = (op ? Yb : Ya) + int64_t(c0) * LFS;
-    const int Mt = geo.M[TL];
-    // interior tile: every mask of the last level is true (no per-word checks)
-    const bool interior = k0 >= 2 * w && k0 + tc * LF <= Mt;
-    // final level: the 5 points of storage quad qi from the three pieces of
-    // the level-(TL-1) window (item5 -> items 5 item5 + e)
-    auto final_quad = [&](const uint32_t *P0, const uint32_t *P1, const uint32_t *P2, int64_t item5, int qi) {
-        const int s0 = qi * 4;
-        const int c = s0 / LFS, r0 = s0 - c * LFS;
-        uint32_t v[5][4];
+    const int64_t Ns = geo.Ns;
+    // final level: the 5 points of every slot's quad from the three pieces of
+    // the level-(TL-1) window of point e (P + e 3 Zp) (items 5 item5 + e')
+    auto final_level = [&](const uint32_t *P, int Zp, int64_t item5) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int j = c * LF + r0 + r, k = k0 + j;
-            const bool data = r0 + r < LF;
-            const bool ka = data && (interior || unsigned(k) < unsigned(Mt));
-            const bool k1 = data && (interior || unsigned(k - w) < unsigned(Mt));
-            const bool k2 = data && (interior || unsigned(k - 2 * w) < unsigned(Mt));
-            const uint32_t a0 = ka ? P0[j + 2 * w] : 0u, a1 = ka ? P1[j + 2 * w] : 0u, a2 = ka ? P2[j + 2 * w] : 0u;
-            const uint32_t s1 = k1 ? P1[j + w] : 0u, s2 = k2 ? P2[j] : 0u;
-            const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
-            v[0][r] = a0;
-            v[1][r] = p1;
-            v[2][r] = a0 ^ xs;
-            v[3][r] = p1 ^ xs;
-            v[4][r] = a2;
+        for (int u = 0; u < FS; ++u) {
+            if (fe[u] < 0) continue;
+            const uint32_t *P0 = P + fe[u] * 3 * Zp, *P1 = P0 + Zp, *P2 = P1 + Zp;
+            uint32_t v[5][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int j = fj0[u] + r, k = k0 + j;
+                const bool data = (fdm[u] >> r) & 1u;
+                const bool ka = data && (interior || unsigned(k) < unsigned(Mt));
+                const bool k1 = data && (interior || unsigned(k - w) < unsigned(Mt));
+                const bool k2 = data && (interior || unsigned(k - 2 * w) < unsigned(Mt));
+                const uint32_t a0 = ka ? P0[j + 2 * w] : 0u, a1 = ka ? P1[j + 2 * w] : 0u,
+                               a2 = ka ? P2[j + 2 * w] : 0u;
+                const uint32_t s1 = k1 ? P1[j + w] : 0u, s2 = k2 ? P2[j] : 0u;
+                const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
+                v[0][r] = a0;
+                v[1][r] = p1;
+                v[2][r] = a0 ^ xs;
+                v[3][r] = p1 ^ xs;
+                v[4][r] = a2;
+            }
+            uint32_t *o = out + ((item5 * 5 + fe[u]) * 5) * Ns + fs0[u];
+#pragma unroll
+            for (int e = 0; e < 5; ++e)
+                *reinterpret_cast<uint4 *>(o + e * Ns) = make_uint4(v[e][0], v[e][1], v[e][2], v[e][3]);
         }
-#pragma unroll
-        for (int e = 0; e < 5; ++e)
-            *reinterpret_cast<uint4 *>(out + (item5 * 5 + e) * geo.Ns + s0) =
-                make_uint4(v[e][0], v[e][1], v[e][2], v[e][3]);
     };
     if constexpr (TL == 1) {
-        for (int qi = tid; qi < nq; qi += kEvalFusedThreads) final_quad(L0, L0 + Z0, L0 + 2 * Z0, g, qi);
+        // TL = 1 has no outer evaluation point: every thread walks the quads
+        for (int qi = tid; qi < nq; qi += kEvalFusedThreads) {
+            const int s0 = qi * 4, c = s0 / LFS, r0 = s0 - c * LFS;
+            uint32_t v[5][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int j = c * LF + r0 + r, k = k0 + j;
+                const bool data = r0 + r < LF;
+                const bool ka = data && unsigned(k) < unsigned(Mt), k1 = data && unsigned(k - w) < unsigned(Mt),
+                           k2 = data && unsigned(k - 2 * w) < unsigned(Mt);
+                const uint32_t a0 = ka ? L0[j + 2 * w] : 0u, a1 = ka ? L0[Z0 + j + 2 * w] : 0u,
+                               a2 = ka ? L0[2 * Z0 + j + 2 * w] : 0u;
+                const uint32_t s1 = k1 ? L0[Z0 + j + w] : 0u, s2 = k2 ? L0[2 * Z0 + j] : 0u;
+                const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
+                v[0][r] = a0;
+                v[1][r] = p1;
+                v[2][r] = a0 ^ xs;
+                v[3][r] = p1 ^ xs;
+                v[4][r] = a2;
+            }
+#pragma unroll
+            for (int e = 0; e < 5; ++e)
+                *reinterpret_cast<uint4 *>(out + (g * 5 + e) * Ns + s0) = make_uint4(v[e][0], v[e][1], v[e][2], v[e][3]);
+        }
     } else if constexpr (TL == 2) {
         constexpr int Z1 = efslot(2, 1);
         uint32_t *L1 = L0 + NP0 * Z0;  // [e1][p2]
@@ -507,11 +554,7 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
         for (int p = 0; p < 3; ++p) sig[p] = p * geo.M[2] + k0 - 2 * w;
         eval_level5(L0, Z0, L1, Z1, 3, (T + 2 * w) >> 2, sig, geo.M[1], tid);
         __syncthreads();
-        for (int it = tid; it < 5 * nq; it += kEvalFusedThreads) {
-            const int e1 = it / nq, qi = it - e1 * nq;
-            const uint32_t *P = L1 + e1 * 3 * Z1;
-            final_quad(P, P + Z1, P + 2 * Z1, g * 5 + e1, qi);
-        }
+        final_level(L1, Z1, g);
     } else {
         static_assert(TL == 3, "1..3 Toom levels");
         constexpr int Z1 = efslot(3, 1), Z2 = efslot(3, 2);
@@ -521,6 +564,7 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
         int sig2[3];
 #pragma unroll
         for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
+        const int M2 = geo.M[2];
 #pragma unroll
         for (int e1 = 0; e1 < 5; ++e1) {
             if (e1 == 0) eval_l1_point<0>(L0, L1, geo, k0, nq1, tid);
@@ -529,13 +573,9 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
             if (e1 == 3) eval_l1_point<3>(L0, L1, geo, k0, nq1, tid);
             if (e1 == 4) eval_l1_point<4>(L0, L1, geo, k0, nq1, tid);
             __syncthreads();
-            eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, geo.M[2], tid);
+            eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, M2, tid);
             __syncthreads();
-            for (int it = tid; it < 5 * nq; it += kEvalFusedThreads) {
-                const int e2 = it / nq, qi = it - e2 * nq;
-                const uint32_t *P = L2 + e2 * 3 * Z2;
-                final_quad(P, P + Z2, P + 2 * Z2, (g * 5 + e1) * 5 + e2, qi);
-            }
+            final_level(L2, Z2, g * 5 + e1);
             // (the next level-1 pass writes only L1; L2 is rewritten after its barrier)
         }
     }
