@@ -942,11 +942,17 @@ toom_interp_assemble(const uint32_t *__restrict__ Q, const uint32_t *__restrict_
     const int ob = int(blockIdx.x - item * nbo);
     const int L = 2 * M;
     const uint32_t *tot = Tot + item * nb * 3 * w;
+    // chain carries = exclusive prefix (over blocks) of the block totals: all
+    // totals loaded by all threads at once (coalesced, independent), then a
+    // short in-shared-memory scan per chain
+    for (int x = threadIdx.x; x < nb * 3 * w; x += blockDim.x) carry[x] = __ldg(tot + x);
+    __syncthreads();
     for (int c = threadIdx.x; c < 3 * w; c += blockDim.x) {
         uint32_t acc = 0;
         for (int b = 0; b < nb; ++b) {
+            const uint32_t v = carry[b * 3 * w + c];
             carry[b * 3 * w + c] = acc;
-            acc ^= __ldg(tot + b * 3 * w + c);
+            acc ^= v;
         }
     }
     __syncthreads();
@@ -1228,7 +1234,9 @@ static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
 
 // Toom interpolation: levels with >= this many products use the one-CTA-per-
 // product kernel (F2X_TOOM_SEQ overrides; measured: 512 products sequential
-// (n=57637 level 1: 263 vs 389 us), 128 two-kernel (n=35851 level 1))
+// (n=57637 level 1: 263 vs 389 us); 128 products: two-kernel in round 1, the
+// sequential form once the node-problem roots became plain (16-byte staging):
+// n=35851 level 1 39 vs 59 us)
 // F2X_TOOM_BLK=2048 pins the sequential interpolation to 2048-coefficient
 // blocks (experiments)
 static int toom_blk_choice() {
@@ -1242,7 +1250,7 @@ static int toom_blk_choice() {
 static int64_t toom_seq_min() {
     static const int64_t v = [] {
         const char *e = getenv("F2X_TOOM_SEQ");
-        return e ? int64_t(atoll(e)) : int64_t(256);
+        return e ? int64_t(atoll(e)) : int64_t(96);
     }();
     return v;
 }
