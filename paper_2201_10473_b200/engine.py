@@ -176,6 +176,56 @@ def clmul64_lanes(a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, torch
     return lohi[:, 0], lohi[:, 1]
 
 
+class CapturedCall:
+    """One batched call on fixed device buffers, captured ONCE as a CUDA graph
+    (every engine launch of the call) and replayed on the caller's current
+    stream: the launch overhead and inter-kernel gaps of a repeated call
+    shrink (measured on B200: n=17669 x 4096 0.329 -> 0.322 ms per call,
+    n=35851 0.902 -> 0.886 ms).  ``kind`` is "cyclic" (``size`` = n) or
+    "full" (``size`` = t); A, B, out are the call's device tensors, read and
+    written in place on every replay; the scratch is owned by the object.
+    For cyclic calls ``err_flag`` accumulates the top-bit rejections."""
+
+    def __init__(self, kind: str, A: torch.Tensor, B: torch.Tensor, out: torch.Tensor, size: int,
+                 leaf: int = 0):
+        if kind not in ("cyclic", "full"):
+            raise ValueError("kind must be 'cyclic' or 'full'")
+        _check_operands(A, B)
+        if not (A.is_contiguous() and B.is_contiguous() and out.is_contiguous()):
+            raise ValueError("captured calls need contiguous buffers")
+        self.kind, self.size, self.leaf = kind, int(size), leaf
+        self.A, self.B, self.out = A, B, out
+        self.device = A.device
+        self.err_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        lib = _lib.load()
+        kind_id = _lib.KIND_CYCLIC if kind == "cyclic" else _lib.KIND_FULL
+        self.ws = torch.empty(max(_row_chunks(lib, kind_id, A.shape[0], self.size, leaf)[1], 256),
+                              dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            s = torch.cuda.Stream(self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                self._call()  # warm: kernel attributes set before capture
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            torch.cuda.synchronize(self.device)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self._call()
+            torch.cuda.synchronize(self.device)
+            self.err_flag.zero_()
+
+    def _call(self):
+        if self.kind == "cyclic":
+            mul_cyclic(self.A, self.B, self.size, out=self.out, leaf=self.leaf, check=False,
+                       err_flag=self.err_flag, workspace=self.ws)
+        else:
+            mul_full(self.A, self.B, out=self.out, leaf=self.leaf, workspace=self.ws)
+
+    def __call__(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out
+
+
 class HostPipeline:
     """Products of HOST-resident operands (pinned torch tensors), end to end.
 

@@ -442,3 +442,34 @@ def test_integration_stub_runs(cuda):
     assert np.array_equal(ns["schoolbook_mul_batch"](A, B), c_mul_full(A, B))
     A, B = make_cyclic_inputs(17669, 40)
     assert np.array_equal(ns["ring_mul_batch"](A, B, 17669), c_mul_cyclic(A, B, 17669))
+
+
+def test_captured_call_replays_exactly(cuda):
+    """engine.CapturedCall (the call captured once as a CUDA graph) gives the
+    oracle's bits on every replay, also after the inputs are rewritten in
+    place, for a ring size, a Toom plan and a full product."""
+    import torch
+
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200.engine import CapturedCall
+
+    for kind, size, batch in (("cyclic", 17669, 96), ("cyclic", 57637, 40), ("full", 64, 70)):
+        if kind == "cyclic":
+            A, B = make_cyclic_inputs(size, 2 * batch)
+            ref = lambda a, b: c_mul_cyclic(a, b, size)  # noqa: E731
+        else:
+            A, B = make_full_inputs(size, 2 * batch, words=True)
+            ref = c_mul_full
+        dA, dB = _dev(A[:batch], cuda), _dev(B[:batch], cuda)
+        out = torch.empty((batch, dA.shape[1] * (2 if kind == "full" else 1)),
+                          dtype=torch.int64, device=cuda)
+        cap = CapturedCall(kind, dA, dB, out, size)
+        for _ in range(2):
+            cap()
+            assert np.array_equal(_np(out), ref(A[:batch], B[:batch])), (kind, size)
+        dA.copy_(_dev(A[batch:], cuda))
+        dB.copy_(_dev(B[batch:], cuda))
+        cap()
+        assert np.array_equal(_np(out), ref(A[batch:], B[batch:])), (kind, size)
+        assert int(cap.err_flag.item()) == 0
