@@ -866,6 +866,11 @@ def main() -> None:
         finally:
             sync.close()
     elif args.gpus > 1:  # spawn one worker per GPU here
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench: --gpus {args.gpus} but only {have} CUDA device(s) visible")
         codes = launch_spawned(args.gpus, _gpu_rank, args)
         bad = [c for c in codes if c != 0]
         if bad:

@@ -144,3 +144,30 @@ def test_bench_two_gpus_spawned(cuda):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["parity"]["ok"]
     assert "NCCL" not in r.stdout + r.stderr
+
+
+def test_random_sizes_vs_oracle(cuda):
+    """Seeded random ring sizes (1 .. 70000 bits, every Toom / leaf / chunk
+    regime the planner reaches) and full-product sizes (1 .. 1536 words)
+    with random batch sizes, against the C oracle."""
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+
+    rng = np.random.default_rng(0x5EED)
+    seen_toom = set()
+    for _ in range(24):
+        n = int(rng.integers(1, 70000))
+        batch = int(rng.integers(1, 48))
+        A, B = make_cyclic_inputs(n, batch)
+        got = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), n))
+        assert np.array_equal(got, c_mul_cyclic(A, B, n)), (n, batch)
+        seen_toom.add(plan("cyclic", batch, n)["toom_levels"])
+    for _ in range(16):
+        t = int(rng.integers(1, 1536))
+        batch = int(rng.integers(1, 40))
+        A, B = make_full_inputs(t, batch, words=True)
+        got = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+        assert np.array_equal(got, c_mul_full(A, B)), (t, batch)
+        seen_toom.add(plan("full", batch, t)["toom_levels"])
+    assert {0, 1, 2} <= seen_toom or {0, 2} <= seen_toom, seen_toom
