@@ -191,7 +191,7 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
 // quad.  Thread x < 2^EL 2 TW owns half-word column x of the tile (one 32x32
 // bit transpose); all threads walk the quads.
 template <int EL>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(8 * 40, 4)  // <= 4 parts x 2 x 40 words; 4 CTAs/SM: one wave at n=17669
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
               int ncyc, uint32_t *d_err, int tiles, int TW) {
@@ -1586,6 +1586,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         const int TW = levels_left >= 6 ? pl.leaf_words : pw;
         const int tiles = pw / TW;
         const int nthr = int(ceil_div((1 << L.el) * 2 * TW, 32) * 32);
+        if (nthr > 8 * 40) return F2X_ERANGE;  // (launch bounds: TW <= LF <= 40)
         dim3 grid(unsigned(G * tiles), 2);
         const size_t sm = size_t(1 << L.el) * (64 * TW + 2 * TW) * 4;
         const size_t sm_max = size_t(1 << L.el) * (64 * kTileWords + 2 * kTileWords) * 4;
