@@ -178,6 +178,62 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     }
 }
 
+// K1 for operands of at most one tile (N <= 4096 coefficients, W =
+// ceil(N/64) words): a CTA of 128 threads slices GPC = 64 / W whole groups at once
+// (thread = (group, half-word column); one tile per group left 75 % of the
+// threads idle at d=1024), and since a group's storage range is its whole
+// operand -- [0, Ns), whole 16-byte quads -- it is written as storage quads.
+__global__ void __launch_bounds__(kTileThreads)
+k1_slice_groups(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
+                uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns, int ncyc,
+                uint32_t *d_err, int64_t G) {
+    __shared__ uint32_t stage[kTileCoeffs + kTileCoeffs / 32];
+    check_poison(stage, sizeof(stage));
+    check_poison_sync();
+    const int tid = threadIdx.x;
+    const int W = (N + 63) >> 6, GPC = kTileWords / W, STG = 64 * W + 2 * W;
+    const int gi = tid / (2 * W), h = tid - gi * (2 * W);
+    const int64_t g = int64_t(blockIdx.x) * GPC + gi;
+    const uint32_t *X = reinterpret_cast<const uint32_t *>(blockIdx.y ? B : A);
+    if (gi < GPC && g < G) {
+        const int u = h >> 1, half = h & 1;
+        uint32_t x[32];
+        uint32_t bad = 0;
+        const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
+                                    ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
+                                    : 0u;
+        const int rows = u < t ? int(batch - g * 32 < 32 ? batch - g * 32 : 32) : 0;
+        const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr) {
+            const uint32_t v = pr < rows ? __ldg(px) : 0u;
+            px += 2 * int64_t(t);
+            bad |= v & himask;
+            x[pr] = v;
+        }
+        if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
+            atomicOr(d_err, uint32_t(bad != 0));
+        transpose32(x);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[gi * STG + stg(32 * h + i)] = x[i];
+    }
+    __syncthreads();
+    // storage quads of the CTA's groups (chunked or plain: LF == LFS == N)
+    const int qpg = int(Ns >> 2), qpc = LFS >> 2;
+    const int64_t g0 = int64_t(blockIdx.x) * GPC;
+    const int ng = int(G - g0 < GPC ? G - g0 : GPC);
+    uint4 *o = reinterpret_cast<uint4 *>((blockIdx.y ? Bbs : Abs) + g0 * Ns);
+    for (int x = tid; x < ng * qpg; x += kTileThreads) {
+        const int gg = x / qpg, q = x - gg * qpg;
+        const int c = q / qpc, r0 = (q - c * qpc) * 4, kb = c * LF + r0;
+        const uint32_t *S = stage + gg * STG;
+        uint32_t v[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) v[rr] = (r0 + rr < LF && kb + rr < N) ? S[stg(kb + rr)] : 0u;
+        o[x] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 // K1 with the top EL global Karatsuba levels pre-evaluated (EL = 1, 2): the
 // CTA transposes the same tile of each of the 2^EL parts of the operand
 // (part j = coefficients [j N/2^EL, (j+1) N/2^EL)) into 2^EL stages, then
@@ -1572,6 +1628,12 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             default: F2X_LAUNCH(toom_eval_fused<3>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
         }
         if ((rc = debug_sync(stream, 2))) return rc;
+    } else if (L.el == 0 && pl.N <= kTileCoeffs) {
+        // one tile per group: several groups per CTA, storage quads
+        const int gpc = kTileWords / int(ceil_div(pl.N, 64));
+        dim3 grid(unsigned(ceil_div(G, gpc)), 2);
+        F2X_LAUNCH(k1_slice_groups, grid, kTileThreads, 0, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
+                   pl.leaf_words, pl.leaf_stride, L.Ns, ncyc, d_err, G);
     } else if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
