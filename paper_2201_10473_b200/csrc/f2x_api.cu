@@ -48,7 +48,7 @@ static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
 static constexpr int kToomW = 16;       // x = X^w (coefficients)
 static constexpr double kToomWordCost = 15.0;  // planner: cost units per word moved (fit on B200)
-static constexpr int kToomMinWords = 544;      // Toom only above 512 words: d=32768 (t=512) measured 4.6 % slower with it
+static constexpr int kToomMinWords = 512;      // Toom from 512 words: d=32768 (t=512) 27.26 -> 25.79 ms with two levels (round 2); t=256 slower (17.90 vs 18.76 ms)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
