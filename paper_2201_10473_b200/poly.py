@@ -284,15 +284,13 @@ def clmul64_batch(a: np.ndarray, b: np.ndarray, counters: Optional[MulCounters] 
 
 
 def _mul_words(aw: np.ndarray, bw: np.ndarray) -> np.ndarray:
-    """One t-word product on the device; returns 2t uint64 words."""
-    import torch
+    """One t-word product on the device (a cached captured call per t:
+    engine.one_product); returns 2t uint64 words."""
+    from .engine import one_product
 
-    from .engine import mul_full
-
-    dev = _device()
-    A = torch.from_numpy(np.ascontiguousarray(aw, dtype=np.uint64).view(np.int64).copy()).reshape(1, -1).to(dev)
-    B = torch.from_numpy(np.ascontiguousarray(bw, dtype=np.uint64).view(np.int64).copy()).reshape(1, -1).to(dev)
-    return mul_full(A, B).cpu().numpy().view(np.uint64)[0].copy()
+    aw = np.ascontiguousarray(aw, dtype=np.uint64)
+    bw = np.ascontiguousarray(bw, dtype=np.uint64)
+    return one_product("full", aw, bw, aw.shape[0], _device())
 
 
 def _convolution_mul_arrays(aw: np.ndarray, bw: np.ndarray, counters: Optional[MulCounters],

@@ -71,19 +71,13 @@ def _params(p) -> RingParams:
 
 def ring_mul(A: PolyWords, B: PolyWords, p) -> PolyWords:
     """A * B mod X^N - 1 for one pair of ceil(N/64)-word operands."""
-    import torch
-
-    from .engine import mul_cyclic
+    from .engine import one_product
     from .poly import _device
 
     rp = _params(p)
     if A.word_len != rp.words or B.word_len != rp.words:
         raise ValueError(f"ring operands need {rp.words} words for N={rp.N}")
-    dev = _device()
-    a = torch.from_numpy(A.words.copy()).reshape(1, -1).to(dev)
-    b = torch.from_numpy(B.words.copy()).reshape(1, -1).to(dev)
-    c = mul_cyclic(a, b, rp.N)
-    return PolyWords(c.cpu().numpy()[0])
+    return PolyWords(one_product("cyclic", A.words, B.words, rp.N, _device()))
 
 
 def ring_mul_batch(A, B, p):
