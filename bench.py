@@ -761,6 +761,8 @@ def gpu_arm(args, sync, local) -> None:
         }
         if scaling:
             line["scaling_57637"] = scaling
+        if getattr(args, "share_device", False):
+            line["functional_test_only"] = "--share-device: all ranks on cuda:0; timings are not a measurement"
         if per_cfg:
             line["per_config"] = per_cfg
         if world == 1 and not args.no_cpu:
@@ -794,7 +796,7 @@ def launch_spawned(world: int, target, *targs, timeout_s: float = 1800.0) -> lis
 
 
 def _gpu_rank(sync, rank, args):
-    gpu_arm(args, sync, rank)
+    gpu_arm(args, sync, 0 if args.share_device else rank)
 
 
 def reference_arm(args) -> None:
@@ -854,6 +856,9 @@ def main() -> None:
     ap.add_argument("--quick", action="store_true", help="headline only (no per-config / scaling lines)")
     ap.add_argument("--no-dsweep", action="store_true", help="skip the configs[4] d-sweep lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--share-device", action="store_true",
+                    help="FUNCTIONAL TEST ONLY: every spawned rank on cuda:0 (exercises the N-rank code "
+                         "path on a one-GPU box; the timings are not a measurement)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "engine":
         args.warmup = 3
@@ -866,14 +871,14 @@ def main() -> None:
             print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
         sync = GlooSync(rank, world) if world > 1 else LocalSync()
         try:
-            gpu_arm(args, sync, local)
+            gpu_arm(args, sync, 0 if args.share_device else local)
         finally:
             sync.close()
     elif args.gpus > 1:  # spawn one worker per GPU here
         import torch
 
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and not args.share_device:
             raise SystemExit(f"bench: --gpus {args.gpus} but only {have} CUDA device(s) visible")
         codes = launch_spawned(args.gpus, _gpu_rank, args)
         bad = [c for c in codes if c != 0]

@@ -123,6 +123,60 @@ def test_odd_offset_row_views(cuda):
     assert np.array_equal(_np(mul_full(dA[:, :4], dB[:, :4])), c_mul_full(A[:, :4], B[:, :4]))
 
 
+def test_bench_two_ranks_spawned_functional(cuda):
+    """The `--gpus 2` spawned-rank path end to end on ONE device
+    (`--share-device`: both ranks on cuda:0; a functional test of the N-rank
+    code -- barrier, max-over-ranks, shard dispatch, scaling block, parity --
+    not a measurement), with no NCCL in the process tree."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NCCL_DEBUG="INFO")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--share-device", "--steps", "5", "--warmup",
+                        "3", "--no-cpu", "--no-dsweep", "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["parity"]["ok"] and line["parity_all_ok"], line
+    assert line["config"]["global_batch"] == 2048 and "functional_test_only" in line
+    sc = line["scaling_57637"]
+    assert sc["n_gpus"] == 2 and [g["rows"] for g in sc["per_gpu"]] == [8192, 8192] and sc["parity"]["ok"]
+    assert "NCCL INFO" not in r.stdout + r.stderr  # no NCCL communicator was created
+
+
+def test_bench_two_ranks_torchrun_functional(cuda):
+    """The torchrun form (the driver's N > 1 launch): two ranks joined by a
+    gloo group for the barrier and the max -- on ONE device
+    (`--share-device`, functional test, not a measurement), no NCCL."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NCCL_DEBUG="INFO")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+                        "--share-device", "--steps", "5", "--warmup", "3", "--no-cpu", "--no-dsweep",
+                        "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["parity_all_ok"] and "GlooSync" in line["config"]["parallelism"]
+    assert "NCCL INFO" not in r.stdout + r.stderr
+
+
 def test_bench_two_gpus_spawned(cuda):
     """`bench.py --gpus 2` without torchrun: two spawned ranks, no NCCL."""
     import json
@@ -143,7 +197,7 @@ def test_bench_two_gpus_spawned(cuda):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["parity"]["ok"]
-    assert "NCCL" not in r.stdout + r.stderr
+    assert "NCCL INFO" not in r.stdout + r.stderr  # no NCCL communicator was created
 
 
 def test_random_sizes_vs_oracle(cuda):
