@@ -16,6 +16,11 @@ Controls (SPEC.md:470-472):
   ``F2X_LEAKY_LEAF`` fixture: leaves skip all-zero a words) -- must FAIL;
 * ``leaky_mul``: a CPU sparse convolution that only visits the set bits of
   A -- must FAIL (``ct_check_leaky``).
+
+``masked=True`` times ``engine.mul_cyclic_masked`` (A*B = (A^R)*B ^ R*B
+with fresh random R): the engine has no data-dependent branch or address,
+but a ~0.1 % physical timing effect of sparse operands (switching power /
+clock management) shows up for some seeds; masking removes it.
 """
 
 from __future__ import annotations
@@ -55,13 +60,19 @@ def _dense_rows(n: int, rows: int, rng) -> np.ndarray:
 
 
 def ct_check(n: int = 17669, weight: int = 75, trials: int = MIN_TRIALS, seed: int = 0xC7,
-             batch: int = 4096, control: bool = False) -> dict:
+             batch: int = 4096, control: bool = False, masked: bool = False) -> dict:
     """GPU fixed-vs-random(dense) timing test of ``mul_cyclic``: the fixed
     first operand is weight-``weight`` sparse, or dense with ``control``.
     ``trials`` calls per class."""
     import torch
 
-    from .engine import mul_cyclic
+    from .engine import mul_cyclic, mul_cyclic_masked
+
+    if masked:
+        gen = torch.Generator(device=torch.device("cuda", torch.cuda.current_device()))
+        gen.manual_seed(seed)
+        mul_cyclic = lambda A, B, n, out, check, err_flag: mul_cyclic_masked(  # noqa: E731
+            A, B, n, out=out, generator=gen, check=check, err_flag=err_flag)
 
     rng = np.random.default_rng(seed)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -98,7 +109,7 @@ def ct_check(n: int = 17669, weight: int = 75, trials: int = MIN_TRIALS, seed: i
     verdict = "pass" if abs(t) < THRESHOLD else "fail"
     if min(len(t_fix), len(t_rnd)) < MIN_TRIALS and verdict == "pass":
         verdict = "inconclusive"  # too few trials to call it constant time
-    return {"n": n, "weight": None if control else weight, "control": control,
+    return {"n": n, "weight": None if control else weight, "control": control, "masked": masked,
             "trials": [len(t_fix), len(t_rnd)],
             "mean_ms": [float(np.mean(t_fix)), float(np.mean(t_rnd))], "t": t, "verdict": verdict}
 

@@ -166,6 +166,33 @@ def mul_cyclic(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | 
     return out
 
 
+def mul_cyclic_masked(A: torch.Tensor, B: torch.Tensor, n: int, *, out: torch.Tensor | None = None,
+                      generator: torch.Generator | None = None, check: bool = True,
+                      err_flag: torch.Tensor | None = None) -> torch.Tensor:
+    """``mul_cyclic`` with the first operand additively masked: with R fresh
+    uniform random ring elements, A*B = (A^R)*B ^ R*B, and both products see
+    uniformly distributed first operands whatever A is.  The engine is
+    constant time by construction (no data-dependent branch or address), but
+    the GPU's switching power -- hence its clocks -- can still depend on the
+    operand bits (a sparse HQC secret toggles fewer bits); masking removes
+    that dependence at twice the work."""
+    _check_operands(A, B)
+    n = int(n)
+    batch, t = A.shape
+    R = torch.randint(-2 ** 31, 2 ** 31, (batch, 2 * t), dtype=torch.int32, device=A.device,
+                      generator=generator).view(torch.int64)
+    r = n - 64 * (t - 1)
+    if r < 64:  # ring elements: bits >= n clear
+        R[:, t - 1] &= (1 << r) - 1
+    flag = err_flag if err_flag is not None else torch.zeros(1, dtype=torch.int32, device=A.device)
+    C1 = mul_cyclic(_rows(A) ^ R, B, n, check=False, err_flag=flag)
+    out = mul_cyclic(R, B, n, out=out, check=False, err_flag=flag)
+    out ^= C1
+    if check and err_flag is None and int(flag.item()) != 0:
+        raise ValueError("operand has bits set at or above n")
+    return out
+
+
 def clmul64_lanes(a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     """Lane-wise 64x64 -> 128 carry-less products (clmul64_batch), device tensors."""
     if a.dim() != 1 or a.shape != b.shape:
