@@ -51,6 +51,11 @@ N_RING = 17669
 BATCH_PER_GPU = 4096
 L2_FLUSH_BYTES = 256 << 20
 RING_CONFIGS = ((12323, 256, "configs[0]"), (35851, 4096, "configs[2]"), (57637, 16384, "configs[3]"))
+# context only (not vs_baseline): the paper's best single-core AVX512 cycle
+# counts as products/s at 2.8 GHz
+PAPER_1CORE = {17669: 2.8e9 / 14872, 35851: 2.8e9 / 46940, 57637: 2.8e9 / 110568,
+               1024: 2.8e9 / 129, 4096: 2.8e9 / 1287, 8192: 2.8e9 / 3977, 16384: 2.8e9 / 12078,
+               32768: 2.8e9 / 36811, 65536: 2.8e9 / 114620}
 SCALE_N, SCALE_BATCH = 57637, 16384
 DSWEEP = (1024, 4096, 8192, 16384, 32768, 65536)
 DSWEEP_OPERAND_BYTES = 1 << 30  # A + B per GPU
@@ -429,6 +434,8 @@ def ring_entry(torch, np, dev, n, batch, label, peak, flush, reps=5, warmup=3) -
                     "levels": p["levels"], "global_levels": p["global_levels"],
                     "eval_levels": p["eval_levels"], "launches": p["launches"]},
            "parity": check_rows(np, "cyclic", n, A, B, dC, parity_rows(batch))}
+    if n in PAPER_1CORE:
+        out["paper_avx512_1core_products_s"] = round(PAPER_1CORE[n], 1)
     del dA, dB, dC
     torch.cuda.empty_cache()
     return out
@@ -465,6 +472,8 @@ def dsweep_entry(torch, np, dev, d, peak, flush, reps=5, warmup=3) -> dict:
                     "workspace_bytes": p["workspace_bytes"], "row_chunks": len(chunks),
                     "ws_budget": _WS_BUDGET},
            "parity": check_rows(np, "full", d, hA, hB, dC, rows)}
+    if d in PAPER_1CORE:
+        out["paper_avx512_1core_products_s"] = round(PAPER_1CORE[d], 1)
     del dA, dB, dC
     torch.cuda.empty_cache()
     return out
@@ -756,6 +765,7 @@ def gpu_arm(args, sync, local) -> None:
                 "note": "analytic counts of the executed plan; W_alg charges 144 t^log2(3)",
             },
             "ncu_node_kernel": committed_ncu(pl),
+            "paper_avx512_1core_products_s": round(PAPER_1CORE[N_RING], 1) if n == N_RING else None,
             "gpu_launches": int(2 * K * pl["launches"]),
             "clocks": cl,
         }
