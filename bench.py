@@ -683,7 +683,8 @@ def gpu_arm(args, sync, local) -> None:
                 "workload": f"ring mul mod X^{SCALE_N}-1 x{SCALE_BATCH} (configs[3])", "n": SCALE_N,
                 "batch": SCALE_BATCH, "ms_per_call": s1["ms_per_call"], "value": s1["value"], "unit": UNIT,
                 "whole_call_frac_int_alu": s1["whole_call_frac_int_alu"], "parity": scaling["parity"],
-                "note": "same measurement as scaling_57637 at N=1"}
+                "note": "same measurement as scaling_57637 at N=1",
+                "paper_avx512_1core_products_s": round(PAPER_1CORE[SCALE_N], 1)}
         if not args.no_dsweep:
             for d in DSWEEP:
                 per_cfg[f"d{d}"] = dsweep_entry(torch, np, dev, d, peak, flush)
