@@ -359,7 +359,9 @@ class HostPipeline:
         self.bounds = [(i, min(i + step, batch)) for i in range(0, batch, step)]
         rows = self.bounds[0][1] - self.bounds[0][0]
         self.lanes = []
-        nstreams = max(1, int(streams))
+        # (no more streams than row chunks: an unused stream would still pin
+        # its buffers and scratch)
+        nstreams = max(1, min(int(streams), len(self.bounds)))
         # every (lane, stream) owns its buffers AND its scratch, sized here
         # once: a captured graph bakes these pointers in, so they must never
         # be shared with (or freed by) other callers of the same stream
