@@ -618,7 +618,10 @@ def gpu_arm(args, sync, local) -> None:
     # several host batches in flight (one pinned buffer set and pipeline lane
     # each) so batch j's H2D/D2H run under batch j-1's kernels; measured on
     # the box (n=17669 x 4096): 1 chunk x 4 lanes 10.6 M/s, 2 x 2 9.7 M/s,
-    # 1 x 2 8.5 M/s (a whole-batch launch keeps the node grid at 23 waves)
+    # 1 x 2 8.5 M/s (a whole-batch launch keeps the node grid at 23 waves);
+    # re-measured on another box (tools/e2e_sweep.py): copy-only ceiling 370
+    # us/batch (11.06 M/s), 2 x 4 388 us, 2 x 6 389, 1 x 4 407, 1 x 6 396 --
+    # the default is 2 chunks x 4 lanes
     LANES = max(1, args.e2e_lanes)
     hAs = [torch.from_numpy(A.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
     hBs = [torch.from_numpy(B.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
@@ -859,7 +862,7 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=N_RING)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--leaf", type=int, default=0)
-    ap.add_argument("--e2e-chunks", type=int, default=1,
+    ap.add_argument("--e2e-chunks", type=int, default=2,
                     help="row chunks per host batch in the e2e pipeline")
     ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
     ap.add_argument("--e2e-lanes", type=int, default=4,
