@@ -90,6 +90,33 @@ __device__ __forceinline__ void chunk_split(int k, int LF, int &c, int &r) {
 // half-word stage index with one pad word per 32 (conflict-free transposes)
 __device__ __forceinline__ int stg(int k) { return k + (k >> 5); }
 
+// K1 load phase: 32 rows (rows < 32 only in a ragged last group; 0 for words
+// u >= t) x one 32-bit half-word column of operand word u (adjacent threads =
+// adjacent halves: coalesced), the ring's constant-time top-bit check on the
+// last word (an OR-reduction into *d_err), the 32x32 transpose.
+// Every branch is on public shape values (batch, t, n, thread index).
+__device__ __forceinline__ void k1_column(const uint32_t *X, int64_t g, int t, int u, int half, int rows,
+                                          int ncyc, uint32_t *d_err, uint32_t (&x)[32]) {
+    const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
+    const int64_t rs = 2 * int64_t(t);
+#pragma unroll
+    for (int pr = 0; pr < 32; ++pr) {
+        x[pr] = pr < rows ? __ldg(px) : 0u;
+        px += rs;
+    }
+    if (ncyc > 0 && u == t - 1) {
+        const int sh = ncyc - 64 * u - 32 * half;  // bits of this half-word below n
+        uint32_t bad = 0;
+        if (sh < 32) {
+            const uint32_t himask = sh <= 0 ? ~0u : ~0u << sh;
+#pragma unroll
+            for (int pr = 0; pr < 32; ++pr) bad |= x[pr] & himask;
+        }
+        if (d_err != nullptr) atomicOr(d_err, uint32_t(bad != 0));
+    }
+    transpose32(x);
+}
+
 // Walk storage words sw = s0 + tid, s0 + tid + 128, ... < s1 of the chunked
 // layout, tracking r = sw mod LFS and the coefficient index kk = chunk*LF + r
 // (relative to kbase) incrementally: one divmod per thread, then adds.
@@ -131,24 +158,9 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
     const uint32_t *X = reinterpret_cast<const uint32_t *>(blockIdx.y ? B : A);
     uint32_t *out = (blockIdx.y ? Bbs : Abs) + g * Ns;
 
-    // load: 32 rows x one 32-bit half-word (adjacent threads = adjacent halves)
     uint32_t x[32];
-    uint32_t bad = 0;
-    const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
-                                ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
-                                : 0u;
     const int rows = u < t ? int(batch - g * 32 < 32 ? batch - g * 32 : 32) : 0;
-    const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
-#pragma unroll
-    for (int pr = 0; pr < 32; ++pr) {
-        const uint32_t v = pr < rows ? __ldg(px) : 0u;
-        px += 2 * int64_t(t);
-        bad |= v & himask;
-        x[pr] = v;
-    }
-    if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
-        atomicOr(d_err, uint32_t(bad != 0));
-    transpose32(x);
+    k1_column(X, g, t, u, half, rows, ncyc, d_err, x);
 #pragma unroll
     for (int i = 0; i < 32; ++i) stage[stg(32 * tid + i)] = x[i];
     __syncthreads();
@@ -183,6 +195,7 @@ k1_slice(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_
 // (thread = (group, half-word column); one tile per group left 75 % of the
 // threads idle at d=1024), and since a group's storage range is its whole
 // operand -- [0, Ns), whole 16-byte quads -- it is written as storage quads.
+template <int Q>  // storage quads per chunk (LFS / 4)
 __global__ void __launch_bounds__(kTileThreads)
 k1_slice_groups(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Abs,
                 uint32_t *__restrict__ Bbs, int64_t batch, int t, int N, int LF, int LFS, int64_t Ns, int ncyc,
@@ -198,39 +211,31 @@ k1_slice_groups(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, 
     if (gi < GPC && g < G) {
         const int u = h >> 1, half = h & 1;
         uint32_t x[32];
-        uint32_t bad = 0;
-        const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
-                                    ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
-                                    : 0u;
         const int rows = u < t ? int(batch - g * 32 < 32 ? batch - g * 32 : 32) : 0;
-        const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
-#pragma unroll
-        for (int pr = 0; pr < 32; ++pr) {
-            const uint32_t v = pr < rows ? __ldg(px) : 0u;
-            px += 2 * int64_t(t);
-            bad |= v & himask;
-            x[pr] = v;
-        }
-        if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
-            atomicOr(d_err, uint32_t(bad != 0));
-        transpose32(x);
+        k1_column(X, g, t, u, half, rows, ncyc, d_err, x);
 #pragma unroll
         for (int i = 0; i < 32; ++i) stage[gi * STG + stg(32 * h + i)] = x[i];
     }
     __syncthreads();
-    // storage quads of the CTA's groups (chunked or plain: LF == LFS == N)
-    const int qpg = int(Ns >> 2), qpc = LFS >> 2;
+    // storage quads of the CTA's groups, chunk c = q / Q at compile time;
+    // (group, quad) advanced incrementally (no division in the loop)
+    const int qpg = int(Ns >> 2);
     const int64_t g0 = int64_t(blockIdx.x) * GPC;
     const int ng = int(G - g0 < GPC ? G - g0 : GPC);
     uint4 *o = reinterpret_cast<uint4 *>((blockIdx.y ? Bbs : Abs) + g0 * Ns);
+    int gg = tid / qpg, q = tid - gg * qpg;
     for (int x = tid; x < ng * qpg; x += kTileThreads) {
-        const int gg = x / qpg, q = x - gg * qpg;
-        const int c = q / qpc, r0 = (q - c * qpc) * 4, kb = c * LF + r0;
+        const int c = q / Q, r0 = (q - c * Q) * 4, kb = c * LF + r0;
         const uint32_t *S = stage + gg * STG;
         uint32_t v[4];
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) v[rr] = (r0 + rr < LF && kb + rr < N) ? S[stg(kb + rr)] : 0u;
+        for (int rr = 0; rr < 4; ++rr) v[rr] = r0 + rr < LF ? S[stg(kb + rr)] : 0u;
         o[x] = make_uint4(v[0], v[1], v[2], v[3]);
+        q += kTileThreads;
+        while (q >= qpg) {
+            q -= qpg;
+            ++gg;
+        }
     }
 }
 
@@ -246,7 +251,7 @@ k1_slice_groups(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, 
 // quads (one 16-byte store per sub-operand and quad) and no two CTAs share a
 // quad.  Thread x < 2^EL 2 TW owns half-word column x of the tile (one 32x32
 // bit transpose); all threads walk the quads.
-template <int EL>
+template <int EL, int Q>  // Q: storage quads per chunk (LFS / 4)
 __global__ void __launch_bounds__(8 * 40, 4)  // <= 4 parts x 2 x 40 words; 4 CTAs/SM: one wave at n=17669
 k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, uint32_t *__restrict__ Ea,
               uint32_t *__restrict__ Eb, int64_t batch, int t, int N, int LF, int LFS, int64_t NsE,
@@ -269,28 +274,14 @@ k1_slice_eval(const uint64_t *__restrict__ A, const uint64_t *__restrict__ B, ui
         const int ul = tile * TW + (h >> 1);  // word within the part
         const int u = j * (NE / 64) + ul;     // operand word
         uint32_t xv[32];
-        uint32_t bad = 0;
-        const uint32_t himask = (ncyc > 0 && u == t - 1 && ncyc - 64 * u - 32 * half < 32)
-                                    ? (ncyc - 64 * u - 32 * half <= 0 ? ~0u : ~0u << (ncyc - 64 * u - 32 * half))
-                                    : 0u;
-        const int r = u < t ? rows : 0;
-        const uint32_t *px = X + ((g * 32) * t + u) * 2 + half;
-#pragma unroll
-        for (int pr = 0; pr < 32; ++pr) {
-            const uint32_t v = pr < r ? __ldg(px) : 0u;
-            px += 2 * int64_t(t);
-            bad |= v & himask;
-            xv[pr] = v;
-        }
-        if (ncyc > 0 && u == t - 1 && d_err != nullptr)  // public condition
-            atomicOr(d_err, uint32_t(bad != 0));
-        transpose32(xv);
+        k1_column(X, g, t, u, half, u < t ? rows : 0, ncyc, d_err, xv);
 #pragma unroll
         for (int i = 0; i < 32; ++i) stage[j * STG + stg(32 * h + i)] = xv[i];
     }
     __syncthreads();
     const int nc = (64 * TW) / LF;  // whole chunks per tile
-    const int qpc = LFS >> 2, nq = nc * qpc;
+    constexpr int qpc = Q;
+    const int nq = nc * qpc;
     uint32_t *out = (blockIdx.y ? Eb : Ea) + g * (NO * NsE) + int64_t(tile) * nc * LFS;
     for (int q = x; q < nq; q += nthr) {
         const int c = q / qpc, r0 = (q - c * qpc) * 4;
@@ -1135,12 +1126,18 @@ k3_interp(const uint32_t *__restrict__ Pin, uint32_t *__restrict__ Pout, int64_t
     for (int m = 0; m < (4 << D); ++m) dst[int64_t(m) * qw] = v[m];
 }
 
-// K4: the tile's 4096 coefficients of the root product are gathered (and,
+// K4: the tile's 64 TW coefficients of the root product are gathered (and,
 // for the ring, folded: c[k] ^= c[k+n]; k >= n zero) into the
-// stage from contiguous storage runs, then thread i transposes half-word i
-// back to 32 rows and stores its 32-bit halves (adjacent threads = adjacent
-// halves of a row: coalesced).
-template <int TW>
+// stage, then thread i transposes half-word i back to 32 rows and stores its
+// 32-bit halves (adjacent threads = adjacent halves of a row: coalesced).
+// QD > 0: chunked root (LF <= 40 data words per chunk, QD = ceil(LF / 4) data
+// quads, chunk stride LFS): gather items are (chunk, data quad) pairs, quad
+// fastest (coalesced 16-byte loads), mapped with compile-time divisions.
+// QD = 0: plain root (coefficient k at word k; Toom plans): items are quads.
+// (Round 2: the per-quad runtime division, the per-word range/pad tests and
+// an always-run zero-fill loop made the old form issue-bound: 1648 warp
+// instructions per tile at d=1024, 81 % issue, 57 % of HBM.)
+template <int TW, int QD>
 __global__ void __launch_bounds__(2 * TW)
 k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64_t batch, int tout,
            int LF, int LFS, int64_t rootStride, int ncyc, int tiles) {
@@ -1154,39 +1151,55 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     const uint32_t *Cg = Croot + g * rootStride;
     const int k0 = tile * TC, kend = min(k0 + TC, 64 * tout);
     const int kvalid = ncyc > 0 ? min(kend, ncyc) : kend;
-    for (int k = k0 + tid; k < k0 + TC; k += TT)
-        if (k >= kvalid) stage[stg(k - k0)] = 0u;
-    // gather root coefficients [ka, kb) into stage index k - ka (XOR when
-    // folding) as 16-byte storage quads; words outside the range or in chunk
-    // pads are skipped (root rows are whole quads: the over-fetch at the ends
-    // stays inside the row)
+    // positions no gather writes (k >= n of the ring, or past the output) are zero
+    for (int k = max(kvalid, k0) + tid; k < k0 + TC; k += TT) stage[stg(k - k0)] = 0u;
+    // gather root coefficients [ka, kb) into stage index k - ka (XOR when folding)
     auto gather = [&](int ka, int kb, bool fold) {
-        int c, r;
-        chunk_split(ka, LF, c, r);
-        const int s0 = c * LFS + r;
-        chunk_split(kb, LF, c, r);
-        const int s1 = c * LFS + r;
         const uint4 *C4 = reinterpret_cast<const uint4 *>(Cg);
-        const int qa = (s0 >> 2) + tid, qb = (s1 + 3) >> 2;
-        // every load of the range in flight at once (one L2/HBM round trip):
-        // <= KQ quads per thread (tile of 64 TW coefficients, <= 1.25 storage
-        // words per coefficient)
-        constexpr int KQ = (64 * TW * 5 / 4 / 4 + TT - 1) / TT + 1;
-        uint4 v[KQ];
+        const int span = kb - ka;
+        if constexpr (QD > 0) {
+            const int c0 = ka / LF, items = ((kb - 1) / LF - c0 + 1) * QD, qs = LFS >> 2;
+            constexpr int NI = (TC / (4 * QD - 3) + 2) * QD / TT + 1;  // items per thread (LF >= 4 QD - 3)
+            uint4 v[NI];
 #pragma unroll
-        for (int i = 0; i < KQ; ++i) v[i] = qa + i * TT < qb ? __ldg(C4 + qa + i * TT) : make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < NI; ++i) {
+                const int it = tid + i * TT, cc = it / QD, iq = it - cc * QD;
+                v[i] = it < items ? __ldg(C4 + (c0 + cc) * qs + iq) : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-        for (int i = 0; i < KQ; ++i) {
-            const int q = qa + i * TT;
-            if (q >= qb) break;
-            const uint32_t vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-            const int sw = 4 * q, cq = sw / LFS, rq = sw - cq * LFS;
-            const int kq = cq * LF + rq - ka;
+            for (int i = 0; i < NI; ++i) {
+                const int it = tid + i * TT, cc = it / QD, iq = it - cc * QD;
+                const int kq = (c0 + cc) * LF + 4 * iq - ka;  // stage index of the quad's first word
+                const uint32_t vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                if (sw + rr >= s0 && sw + rr < s1 && rq + rr < LF) {
-                    if (fold) stage[stg(kq + rr)] ^= vv[rr];
-                    else stage[stg(kq + rr)] = vv[rr];
+                for (int j = 0; j < 4; ++j) {
+                    const int kk = kq + j;
+                    if (it < items && 4 * iq + j < LF && unsigned(kk) < unsigned(span)) {
+                        if (fold) stage[stg(kk)] ^= vv[j];
+                        else stage[stg(kk)] = vv[j];
+                    }
+                }
+            }
+        } else {
+            const int q0 = ka >> 2, items = ((kb + 3) >> 2) - q0;  // root rows are whole quads
+            constexpr int NI = (TC / 4 + 1 + TT - 1) / TT;
+            uint4 v[NI];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int it = tid + i * TT;
+                v[i] = it < items ? __ldg(C4 + q0 + it) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int it = tid + i * TT, kq = 4 * (q0 + it) - ka;
+                const uint32_t vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int kk = kq + j;
+                    if (it < items && unsigned(kk) < unsigned(span)) {
+                        if (fold) stage[stg(kk)] ^= vv[j];
+                        else stage[stg(kk)] = vv[j];
+                    }
                 }
             }
         }
@@ -1205,10 +1218,14 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     if (u < tout) {
         const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
         uint32_t *po = reinterpret_cast<uint32_t *>(out) + ((g * 32) * tout + u) * 2 + (tid & 1);
+        const int64_t rs = 2 * int64_t(tout);
+        if (rows == 32) {
 #pragma unroll
-        for (int pr = 0; pr < 32; ++pr) {
-            if (pr < rows) *po = x[pr];
-            po += 2 * int64_t(tout);
+            for (int pr = 0; pr < 32; ++pr) po[pr * rs] = x[pr];
+        } else {
+#pragma unroll
+            for (int pr = 0; pr < 32; ++pr)
+                if (pr < rows) po[pr * rs] = x[pr];
         }
     }
 }
@@ -1632,8 +1649,16 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         // one tile per group: several groups per CTA, storage quads
         const int gpc = kTileWords / int(ceil_div(pl.N, 64));
         dim3 grid(unsigned(ceil_div(G, gpc)), 2);
-        F2X_LAUNCH(k1_slice_groups, grid, kTileThreads, 0, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
-                   pl.leaf_words, pl.leaf_stride, L.Ns, ncyc, d_err, G);
+#define F2X_K1G(Q) F2X_LAUNCH(k1_slice_groups<Q>, grid, kTileThreads, 0, stream, A, B, Abs, Bbs, batch, pl.t, \
+                               pl.N, pl.leaf_words, pl.leaf_stride, L.Ns, ncyc, d_err, G)
+        switch (pl.leaf_stride / 4) {  // storage quads per chunk (odd: 5, 7, 9, 11)
+            case 5: F2X_K1G(5); break;
+            case 7: F2X_K1G(7); break;
+            case 9: F2X_K1G(9); break;
+            case 11: F2X_K1G(11); break;
+            default: return F2X_ERANGE;
+        }
+#undef F2X_K1G
     } else if (L.el == 0) {
         const int tiles = int(ceil_div(pl.N, kTileCoeffs));
         dim3 grid(unsigned(G * tiles), 2);
@@ -1652,25 +1677,39 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         dim3 grid(unsigned(G * tiles), 2);
         const size_t sm = size_t(1 << L.el) * (64 * TW + 2 * TW) * 4;
         const size_t sm_max = size_t(1 << L.el) * (64 * kTileWords + 2 * kTileWords) * 4;
-        static std::atomic<uint32_t> attr_dev_mask[3];  // per EL: devices configured
+        const int Qc = pl.leaf_stride / 4;  // storage quads per chunk (odd: 5, 7, 9, 11)
+        const int qi = Qc == 5 ? 0 : Qc == 7 ? 1 : Qc == 9 ? 2 : Qc == 11 ? 3 : -1;
+        if (qi < 0) return F2X_ERANGE;
+        static std::atomic<uint32_t> attr_dev_mask[3][4];  // per (EL, Q): devices configured
         int dev = 0;
         cudaGetDevice(&dev);
-        if (dev < 31 && !(attr_dev_mask[L.el].load() & (1u << dev))) {
-            const cudaError_t ae = L.el == 1
-                ? cudaFuncSetAttribute(k1_slice_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max))
-                : cudaFuncSetAttribute(k1_slice_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max));
-            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
-            attr_dev_mask[L.el].fetch_or(1u << dev);
-        }
+#define F2X_K1E(EL, Q)                                                                                       \
+    do {                                                                                                     \
+        if (dev < 31 && !(attr_dev_mask[EL][qi].load() & (1u << dev))) {                                     \
+            const cudaError_t ae = cudaFuncSetAttribute(k1_slice_eval<EL, Q>,                                \
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_max)); \
+            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);                                               \
+            attr_dev_mask[EL][qi].fetch_or(1u << dev);                                                       \
+        }                                                                                                    \
+        F2X_LAUNCH((k1_slice_eval<EL, Q>), grid, nthr, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,        \
+                   pl.leaf_words, pl.leaf_stride, L.Ns >> EL, ncyc, d_err, tiles, TW);                       \
+    } while (0)
         if (L.el == 1) {
-            F2X_LAUNCH(k1_slice_eval<1>, grid, nthr, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
-                                                                 pl.leaf_words, pl.leaf_stride,
-                                                                 L.Ns >> 1, ncyc, d_err, tiles, TW);
+            switch (Qc) {
+                case 5: F2X_K1E(1, 5); break;
+                case 7: F2X_K1E(1, 7); break;
+                case 9: F2X_K1E(1, 9); break;
+                default: F2X_K1E(1, 11); break;
+            }
         } else {
-            F2X_LAUNCH(k1_slice_eval<2>, grid, nthr, sm, stream, A, B, Abs, Bbs, batch, pl.t, pl.N,
-                                                                 pl.leaf_words, pl.leaf_stride,
-                                                                 L.Ns >> 2, ncyc, d_err, tiles, TW);
+            switch (Qc) {
+                case 5: F2X_K1E(2, 5); break;
+                case 7: F2X_K1E(2, 7); break;
+                case 9: F2X_K1E(2, 9); break;
+                default: F2X_K1E(2, 11); break;
+            }
         }
+#undef F2X_K1E
     }
     if ((rc = debug_sync(stream, 1))) return rc;
     // K2
@@ -1787,8 +1826,24 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         // under one wave at 64 words)
         constexpr int TW4 = 32;
         const int tiles = int(ceil_div(tout, TW4));
-        F2X_LAUNCH(k4_unslice<TW4>, unsigned(G * tiles), 2 * TW4, 0, stream, 
-            root, C, batch, tout, rootLF, rootLFS, rootS, ncyc, tiles);
+        const unsigned grid = unsigned(G * tiles);
+#define F2X_K4(QD) F2X_LAUNCH((k4_unslice<TW4, QD>), grid, 2 * TW4, 0, stream, root, C, batch, tout, rootLF, \
+                               rootLFS, rootS, ncyc, tiles)
+        if (rootLF == rootLFS) {
+            F2X_K4(0);  // plain root
+        } else {
+            switch ((rootLF + 3) / 4) {  // data quads per chunk (LF 16..40)
+                case 4: F2X_K4(4); break;
+                case 5: F2X_K4(5); break;
+                case 6: F2X_K4(6); break;
+                case 7: F2X_K4(7); break;
+                case 8: F2X_K4(8); break;
+                case 9: F2X_K4(9); break;
+                case 10: F2X_K4(10); break;
+                default: return F2X_ERANGE;
+            }
+        }
+#undef F2X_K4
     }
     if ((rc = debug_sync(stream, 4))) return rc;
     const cudaError_t ce = cudaGetLastError();
