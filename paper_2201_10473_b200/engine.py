@@ -34,6 +34,23 @@ def _workspace(device: torch.device, stream: torch.cuda.Stream, nbytes: int) -> 
         return ws
 
 
+def release_workspaces(device: int | torch.device | None = None) -> int:
+    """Drop the cached per-(device, stream) scratch (all devices, or one):
+    the next call on a stream allocates afresh.  Synchronises the device(s)
+    first, since queued work may still use the buffers.  Returns the bytes
+    released (``torch.cuda.empty_cache()`` then returns them to the driver).
+    CapturedCall / HostPipeline own their scratch and are not affected."""
+    idx = None if device is None else torch.device("cuda", device).index if isinstance(device, int) \
+        else torch.device(device).index
+    freed = 0
+    with _ws_lock:
+        for key in [k for k in _workspaces if idx is None or k[0] == idx]:
+            if torch.cuda.is_available():
+                torch.cuda.synchronize(key[0])
+            freed += _workspaces.pop(key).numel()
+    return freed
+
+
 # Scratch budget per call: larger batches run as consecutive row chunks (whole
 # 32-row groups) on the same stream, so memory stays bounded; F2X_WS_BUDGET
 # (bytes) overrides the default of 8 GiB.

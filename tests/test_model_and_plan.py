@@ -360,3 +360,23 @@ def test_row_chunks_bound_workspace(monkeypatch):
         assert b == c and (b - a) % 32 == 0
     monkeypatch.setattr(engine, "_WS_BUDGET", 8 << 30)
     assert engine._row_chunks(lib, _lib.KIND_CYCLIC, 4096, 17669, 0)[0] == [(0, 4096)]
+
+
+def test_release_workspaces_drops_cached_scratch():
+    """engine.release_workspaces empties the grow-only per-(device, stream)
+    scratch cache (all devices or one) and reports the bytes dropped."""
+    import torch
+
+    from paper_2201_10473_b200 import engine
+
+    saved = dict(engine._workspaces)
+    try:
+        engine._workspaces.clear()
+        engine._workspaces[(0, 1)] = torch.empty(100, dtype=torch.uint8)
+        engine._workspaces[(1, 7)] = torch.empty(30, dtype=torch.uint8)
+        if not torch.cuda.is_available():
+            assert engine.release_workspaces(1) == 30 and list(engine._workspaces) == [(0, 1)]
+            assert engine.release_workspaces() == 100 and not engine._workspaces
+    finally:
+        engine._workspaces.clear()
+        engine._workspaces.update(saved)
