@@ -781,18 +781,39 @@ toom_interp_scan(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ Q, uin
     }
 }
 
+// Resident-root form (RES, the innermost Toom level of a plan whose last
+// global Karatsuba pass is a single level, n=57637): the CTA first builds its
+// five node-problem roots in shared memory straight from their three path
+// products each (the k3_interp<1> recombination, per storage quad w of a
+// path product: root octant m = 0..7 from the quarters lo_q, hi_q, mid_q at
+// w), then walks the blocks reading the roots in place -- no staging and no
+// root round trip through HBM (k3_interp<1> wrote and this level re-read
+// 2.3 GB per n=57637 call).  Path product c (0 lo, 1 hi, 2 mid) of node
+// problem np is at P + (3 np + c) inS, chunked (LF, LFS), quarters of qw
+// storage words; root octants have oc = (qw / LFS) LF coefficients.
+struct KRootIn {
+    const uint32_t *P;
+    int64_t inS;
+    int qw, oc, LF, LFS;
+    int hp;  // resident root stride in shared memory, words
+};
+// resident root index of coefficient k (k >= -2w): tstg layout, 2w halo
+__host__ __device__ constexpr int kres_words(int nb, int blk) {
+    return (nb * blk + 3 * kToomW) + 16 * (((nb * blk + 3 * kToomW) >> 7) + 1);
+}
+
 // Single-kernel variant: one CTA per item walks its blocks in order, so the
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
 // XORed after a barrier): no c_j round trip through HBM, one launch.
-template <int BLK>
-__global__ void __launch_bounds__(kToomScanT, 3)
+template <int BLK, bool RES>
+__global__ void __launch_bounds__(kToomScanT, RES ? 2 : 3)
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
-                int Lin, int64_t outS) {
+                int Lin, int64_t outS, const KRootIn kr) {
     extern __shared__ uint32_t tsm[];
     constexpr int W = kToomW, ROWS = BLK / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
     constexpr int H = BLK + 3 * W;
-    constexpr int HP = toom_stg_stride(BLK);  // padded stride per input (see tstg)
+    const int HP = RES ? kr.hp : toom_stg_stride(BLK);  // padded stride per input (see tstg)
     uint32_t *Stg = tsm;  // [5][HP]
     __shared__ uint32_t stot[3][NSEG][W];
     __shared__ uint32_t bcar[3][W];  // carry into the current block, per chain
@@ -802,6 +823,52 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
     check_poison_sync();
     const int64_t item = blockIdx.x;
     const int L = 2 * M, nb = (L + BLK - 1) / BLK;
+    if constexpr (RES) {
+        // roots -> Stg[e HP + tstg(k + 2w)], k in [-2w, nb BLK + w); zero outside [0, Lin)
+        const int span = nb * BLK + 3 * W;  // resident slots h = k + 2w the block walk reads
+        for (int h = int(threadIdx.x); h < span; h += kToomScanT) {
+            const int k = h - 2 * W;
+            if (k < 0 || k >= Lin) {
+#pragma unroll
+                for (int e = 0; e < 5; ++e) Stg[e * HP + tstg(h)] = 0u;
+            }
+        }
+        const int q4 = kr.qw >> 2, qsz = kr.LFS >> 2;  // quads per quarter / per chunk
+        const uint4 *P4 = reinterpret_cast<const uint4 *>(kr.P + item * 15 * kr.inS);
+        const int64_t cs = kr.inS >> 2;  // path-product stride, quads
+#pragma unroll 1  // (2-3 items in flight per thread measured 4-16 % slower)
+        for (int x = int(threadIdx.x); x < 5 * q4; x += kToomScanT) {
+            const int e = x / q4, wq = x - e * q4;
+            const uint4 *lo = P4 + (3 * e) * cs + wq, *hi = lo + cs, *mid = hi + cs;
+            uint4 l[4], hh[4], m[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                l[q] = __ldg(lo + q * q4);
+                hh[q] = __ldg(hi + q * q4);
+                m[q] = __ldg(mid + q * q4);
+            }
+            uint4 o[8];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {  // k3_rec<1>
+                const uint4 T = l[2 + i] ^ hh[i];
+                o[i] = l[i];
+                o[2 + i] = xor3(T, l[i], m[i]);
+                o[4 + i] = xor3(T, hh[2 + i], m[2 + i]);
+                o[6 + i] = hh[2 + i];
+            }
+            const int c = wq / qsz, r0 = 4 * (wq - c * qsz);  // chunk, first word in it
+            const int kq = c * kr.LF + r0 + 2 * W;             // resident index of octant 0's first word
+            uint32_t *S0 = Stg + e * HP;
+#pragma unroll
+            for (int mo = 0; mo < 8; ++mo) {
+                const uint32_t vv[4] = {o[mo].x, o[mo].y, o[mo].z, o[mo].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (r0 + j < kr.LF) S0[tstg(kq + mo * kr.oc + j)] = vv[j];
+            }
+        }
+        __syncthreads();
+    }
     const ToomIn in{Cin + item * 5 * inS, inS, LFi, LFSi, Lin, 1.0f / float(LFi)};
     uint32_t *Rg = R + item * outS;
     const bool plain = LFi == LFSi;
@@ -814,7 +881,9 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
 #pragma unroll 1
     for (int b = 0; b < nb; ++b) {
         const int k0 = b * BLK, kb = k0 - 2 * W;
-        if (vec) {  // plain, 16-byte aligned inputs: quads, all in flight per half
+        if constexpr (RES) {
+            __syncthreads();  // previous block's readers of stot / bcar are done
+        } else if (vec) {  // plain, 16-byte aligned inputs: quads, all in flight per half
             constexpr int T = kToomScanT, H4 = H / 4, NQ = (5 * H4 + T - 1) / T, NH = (NQ + 1) / 2;
             __syncthreads();  // previous block's readers of Stg / stot are done
 #pragma unroll
@@ -890,16 +959,16 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
                 }
             }
         }
-        __syncthreads();
-        auto S = [&](int e, int k) -> uint32_t { return Stg[e * HP + tstg(k - kb)]; };
-        const int kr = k0 + sg * SEGR * W + r;
+        if constexpr (!RES) __syncthreads();
+        auto S = [&](int e, int k) -> uint32_t { return Stg[e * HP + tstg(RES ? k + 2 * W : k - kb)]; };
+        const int kr0 = k0 + sg * SEGR * W + r;
         uint32_t v1[SEGR], v2[SEGR], v3[SEGR];
         {
             uint32_t a1 = 0, a2 = 0, a3 = 0;
-            uint32_t cx = S(2, kr), cx1 = S(3, kr);
+            uint32_t cx = S(2, kr0), cx1 = S(3, kr0);
 #pragma unroll
             for (int i = 0; i < SEGR; ++i) {
-                const int k = kr + i * W;
+                const int k = kr0 + i * W;
                 const uint32_t c0w = S(0, k + W), c1w = S(1, k + W), cxw = S(2, k + W), cx1w = S(3, k + W);
                 a1 ^= c0w ^ cxw ^ cx ^ cx1;
                 a2 ^= c1w ^ cx ^ cx1w ^ cx1;
@@ -926,10 +995,10 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         // in registers for the read-modify-write after the barrier
         uint32_t keep[SEGR][4];
         {
-            uint32_t c4m2 = S(4, kr - 2 * W), c4m1 = S(4, kr - W);
+            uint32_t c4m2 = S(4, kr0 - 2 * W), c4m1 = S(4, kr0 - W);
 #pragma unroll
             for (int i = 0; i < SEGR; ++i) {
-                const int k = kr + i * W;
+                const int k = kr0 + i * W;
                 const uint32_t c0 = S(0, k), c4 = S(4, k), c4w = c4m1 ^ c4m2;
                 const uint32_t cj[5] = {c0, v1[i] ^ g1 ^ c0 ^ S(1, k) ^ c4w, v2[i] ^ g2 ^ c4 ^ c4w, v3[i] ^ g3, c4};
                 if (k < L) {
@@ -955,13 +1024,13 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             uint32_t old[HB][4];
 #pragma unroll
             for (int i = 0; i < HB; ++i) {
-                const int k = kr + (h2 + i) * W;
+                const int k = kr0 + (h2 + i) * W;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) old[i][j] = (h2 + i < SEGR && k < L && k >= M) ? Rg[k + j * M] : 0u;
             }
 #pragma unroll
             for (int i = 0; i < HB; ++i) {
-                const int k = kr + (h2 + i) * W;
+                const int k = kr0 + (h2 + i) * W;
                 if (h2 + i < SEGR && k < L && k >= M) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ keep[h2 + i][j];
@@ -1338,6 +1407,38 @@ static bool toom_use_seq(int64_t items, int64_t M) {
     return items >= toom_seq_min() || nb * 3 * kToomW * 4 > 48 * 1024;
 }
 
+// Block size of a one-CTA-per-product interpolation level: 2304-coefficient
+// blocks (9 rows per scan segment) cost ~10 % more per coefficient than 2048
+// (8 rows), so they are taken only when they stage clearly fewer
+// coefficients: n=57637 level 3 (2M = 4300: 2 blocks instead of 3, 704 ->
+// 592 us); levels 1-2 measured 4-10 % slower with 2304
+static int toom_seq_blk(int64_t M) {
+    const int64_t nb2048 = ceil_div(2 * M, 2048), nb2304 = ceil_div(2 * M, 2304);
+    return double(nb2304) * 2304 * 1.1 < double(nb2048) * 2048 && toom_blk_choice() != 2048 ? 2304 : 2048;
+}
+
+// Resident-root interpolation (toom_interp_seq<BLK, true>): the last global
+// pass, when it is a single Karatsuba level into the node-problem root, is
+// folded into the innermost Toom level if that level runs one CTA per
+// product and its five roots fit in shared memory (2 CTAs/SM).
+// F2X_KROOT=0 keeps the separate k3_interp<1> pass (A/B).
+static constexpr int kResSmemMax = 110 * 1024;
+static bool kroot_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("F2X_KROOT");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+static int kroot_hp(int64_t M) {  // resident root stride (words)
+    const int blk = toom_seq_blk(M);
+    return kres_words(int(ceil_div(2 * M, blk)), blk);
+}
+static bool kroot_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int64_t M_TL) {
+    return kroot_enabled() && TL > 0 && np > 0 && pass_levels[np - 1] == 1 &&
+           toom_use_seq(G * ipow5(TL - 1), M_TL) && int64_t(5) * kroot_hp(M_TL) * 4 <= kResSmemMax;
+}
+
 // F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
 static int toom_override() {
     static const int v = [] {
@@ -1427,7 +1528,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         rem -= p;
     }
     pl->num_passes = np;
-    pl->launches = 3 + np + 2 * TL;
+    pl->launches = 3 + np + 2 * TL - (kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ? 1 : 0);
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
@@ -1730,8 +1831,23 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     uint32_t *cur = P0, *nxt = P1;
     int d = pl.global_levels;
     const int64_t in_stride0 = 2 * (L.Ns >> d);  // node products
+    // last pass folded into the innermost Toom interpolation (resident roots)
+    const bool kroot = kroot_fused(L.tl, pl.num_passes, pl.pass_levels, G, L.M[L.tl]);
+    KRootIn kr{};
     for (int i = 0; i < pl.num_passes; ++i) {
         const int D = pl.pass_levels[i];
+        if (kroot && i == pl.num_passes - 1) {  // D = 1 into the root
+            const int64_t Shi = L.Ns >> d;
+            kr.P = cur;
+            kr.inS = i == 0 ? in_stride0 : 2 * Shi;
+            kr.qw = int(Shi / 2);
+            kr.oc = kr.qw / pl.leaf_stride * pl.leaf_words;
+            kr.LF = pl.leaf_words;
+            kr.LFS = pl.leaf_stride;
+            kr.hp = kroot_hp(L.M[L.tl]);
+            d -= D;
+            break;
+        }
         const int dlo = d - D;
         const int64_t Shi = L.Ns >> d, Slo = L.Ns >> dlo;
         const int qw = int(Shi / 2);
@@ -1760,7 +1876,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     const uint32_t *root = cur;
     int rootLF = pl.leaf_words, rootLFS = pl.leaf_stride;
     int64_t rootS = pl.num_passes == 0 ? in_stride0 : 2 * L.Ns;
-    if (L.tl > 0 && pl.num_passes > 0) {  // plain root (last K3 pass above)
+    if (L.tl > 0 && pl.num_passes > 0 && !kroot) {  // plain root (last K3 pass above)
         rootS = 2 * (int64_t(pl.leaf_words) << pl.levels);
         rootLF = rootLFS = int(rootS);
     }
@@ -1783,27 +1899,39 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
             cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sms));
             if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                ae = cudaFuncSetAttribute(toom_interp_seq<2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(5 * toom_stg_stride(2048) * 4));
             if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2304>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                ae = cudaFuncSetAttribute(toom_interp_seq<2304, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(5 * toom_stg_stride(2304) * 4));
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_interp_seq<2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kResSmemMax);
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_interp_seq<2304, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kResSmemMax);
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             attr_dev_mask.fetch_or(1u << dev);
         }
         if (seq) {
-            // block size per level: 2304-coefficient blocks (9 rows per scan
-            // segment) cost ~10 % more per coefficient than 2048 (8 rows), so
-            // they are taken only when they stage clearly fewer coefficients:
-            // n=57637 level 3 (2M = 4300: 2 blocks instead of 3, 704 -> 592
-            // us); levels 1-2 measured 4-10 % slower with 2304
-            const int64_t nb2048 = ceil_div(2 * M, 2048), nb2304 = ceil_div(2 * M, 2304);
-            if (double(nb2304) * 2304 * 1.1 < double(nb2048) * 2048 && toom_blk_choice() != 2048) {
-                F2X_LAUNCH(toom_interp_seq<2304>, unsigned(items), kToomScanT, 5 * toom_stg_stride(2304) * 4, stream, 
-                    root, out, M, rootLF, rootLFS, rootS, Lin, outS);
+            const bool res = kroot && l == L.tl;  // roots built in shared memory from the path products
+            const size_t smr = res ? size_t(5) * kr.hp * 4 : 0;
+            if (toom_seq_blk(M) == 2304) {
+                if (res)
+                    F2X_LAUNCH((toom_interp_seq<2304, true>), unsigned(items), kToomScanT, smr, stream, root, out, M,
+                               rootLF, rootLFS, rootS, Lin, outS, kr);
+                else
+                    F2X_LAUNCH((toom_interp_seq<2304, false>), unsigned(items), kToomScanT,
+                               5 * toom_stg_stride(2304) * 4, stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS,
+                               kr);
             } else {
-                F2X_LAUNCH(toom_interp_seq<2048>, unsigned(items), kToomScanT, 5 * toom_stg_stride(2048) * 4, stream, 
-                    root, out, M, rootLF, rootLFS, rootS, Lin, outS);
+                if (res)
+                    F2X_LAUNCH((toom_interp_seq<2048, true>), unsigned(items), kToomScanT, smr, stream, root, out, M,
+                               rootLF, rootLFS, rootS, Lin, outS, kr);
+                else
+                    F2X_LAUNCH((toom_interp_seq<2048, false>), unsigned(items), kToomScanT,
+                               5 * toom_stg_stride(2048) * 4, stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS,
+                               kr);
             }
             if ((rc = debug_sync(stream, 5))) return rc;
         } else {

@@ -380,3 +380,18 @@ def test_release_workspaces_drops_cached_scratch():
     finally:
         engine._workspaces.clear()
         engine._workspaces.update(saved)
+
+
+def test_plan_resident_root_launches(lib):
+    """The last global Karatsuba pass of a Toom plan (one level into the
+    node-problem root) is folded into the innermost Toom interpolation
+    (resident roots) when that level runs one CTA per product (>= 96
+    products): one launch fewer.  n=35851's last pass has two levels."""
+    from paper_2201_10473_b200 import _lib
+
+    for batch, fused in ((16384, True), (160, True), (40, False)):
+        pl = _lib.make_plan(_lib.KIND_CYCLIC, batch, 57637)
+        assert pl.toom_levels == 3 and pl.num_passes == 1 and pl.pass_levels[0] == 1
+        assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels - (1 if fused else 0), batch
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 35851)
+    assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels
