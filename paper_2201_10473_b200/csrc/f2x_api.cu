@@ -1299,6 +1299,62 @@ k4_unslice(const uint32_t *__restrict__ Croot, uint64_t *__restrict__ out, int64
     }
 }
 
+// K3 (last pass) + K4 in one CTA per group (Karatsuba-only plans with many
+// groups, the configs[4] d-sweep): the group's root is rebuilt by the last
+// global interpolation pass (k3_rec<D> per quarter index w, all 4 2^D root
+// slabs of that w) straight into a shared stage in coefficient order (the
+// K4 stage layout; the ring's fold XORs coefficient k >= n onto k - n), then
+// every thread transposes half-word columns back to rows as in K4.  The root
+// never goes through HBM (d=4096: 1.2 GB written and re-read per call).
+constexpr int kK34Threads = 256;
+template <int D>
+__global__ void __launch_bounds__(kK34Threads, D <= 2 ? 4 : 2)  // D <= 3 (see k34_fused)
+k34_root_unslice(const uint32_t *__restrict__ Pin, uint64_t *__restrict__ out, int64_t batch, int tout, int qw,
+                 int64_t inStride, int LF, int LFS, int ncyc) {
+    extern __shared__ uint32_t stage[];  // [stg(64 tout)]
+    const int KS = 64 * tout;            // output coefficients
+    check_poison(stage, unsigned(stg(KS) * 4));
+    check_poison_sync();
+    const int tid = threadIdx.x;
+    const int64_t g = blockIdx.x;
+    if (ncyc > 0) {  // the fold accumulates: zero first
+        for (int k = tid; k < KS; k += kK34Threads) stage[stg(k)] = 0u;
+        __syncthreads();
+    }
+    const int qc = qw / LFS;  // chunks per root slab
+#pragma unroll 1
+    for (int w = tid; w < qw; w += kK34Threads) {
+        uint32_t v[4 << D];
+        k3_rec<D>(v, Pin, inStride, g, qw, w);
+        const int cw = w / LFS, r = w - cw * LFS;
+        if (r < LF) {
+#pragma unroll
+            for (int m = 0; m < (4 << D); ++m) {
+                const int k = (m * qc + cw) * LF + r;  // root coefficient
+                if (ncyc > 0) {
+                    if (k < 2 * ncyc) atomicXor(&stage[stg(k < ncyc ? k : k - ncyc)], v[m]);
+                } else if (k < KS) {
+                    stage[stg(k)] = v[m];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int rows = int(batch - g * 32 < 32 ? batch - g * 32 : 32);
+#pragma unroll 1
+    for (int h = tid; h < 2 * tout; h += kK34Threads) {
+        uint32_t x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = stage[stg(32 * h + i)];
+        transpose32(x);
+        uint32_t *po = reinterpret_cast<uint32_t *>(out) + (g * 32) * 2 * int64_t(tout) + h;
+        const int64_t rs = 2 * int64_t(tout);
+#pragma unroll
+        for (int pr = 0; pr < 32; ++pr)
+            if (pr < rows) po[pr * rs] = x[pr];
+    }
+}
+
 // ---------------------------------------------------------------- planner
 
 struct Layout {
@@ -1434,6 +1490,26 @@ static int kroot_hp(int64_t M) {  // resident root stride (words)
     const int blk = toom_seq_blk(M);
     return kres_words(int(ceil_div(2 * M, blk)), blk);
 }
+// Last global pass + K4 fused (k34_root_unslice): Karatsuba-only plans with
+// enough groups to fill the GPU with one CTA per group and a root stage that
+// fits shared memory.  F2X_K34=0 keeps the separate passes (A/B).
+// Measured (d-sweep, µs): D = 2 (d=4096) k3 571 + K4 369 -> 768; D = 3
+// (d=8192) 762 + 368 -> 1050; D = 4 (d=16384, 135 KB stage, 1 CTA/SM) 1064 +
+// 369 -> 1955 -- so only up to three levels and two CTAs per SM.
+static constexpr int64_t kK34MinGroups = 1024;
+static constexpr int kK34SmemMax = 72 * 1024;
+static bool k34_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("F2X_K34");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+static bool k34_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int tout) {
+    const int64_t ks = 64 * int64_t(tout);
+    return k34_enabled() && TL == 0 && np > 0 && pass_levels[np - 1] <= 3 && G >= kK34MinGroups &&
+           (ks + ks / 32) * 4 <= kK34SmemMax;
+}
 static bool kroot_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int64_t M_TL) {
     return kroot_enabled() && TL > 0 && np > 0 && pass_levels[np - 1] == 1 &&
            toom_use_seq(G * ipow5(TL - 1), M_TL) && int64_t(5) * kroot_hp(M_TL) * 4 <= kResSmemMax;
@@ -1528,7 +1604,8 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         rem -= p;
     }
     pl->num_passes = np;
-    pl->launches = 3 + np + 2 * TL - (kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ? 1 : 0);
+    pl->launches = 3 + np + 2 * TL - (kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ? 1 : 0) -
+                   (k34_fused(TL, np, pl->pass_levels, G, kind == F2X_KIND_FULL ? 2 * t : t) ? 1 : 0);
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
     pl->node_smem_bytes = int64_t(e->smem);
@@ -1834,8 +1911,20 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     // last pass folded into the innermost Toom interpolation (resident roots)
     const bool kroot = kroot_fused(L.tl, pl.num_passes, pl.pass_levels, G, L.M[L.tl]);
     KRootIn kr{};
+    const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
+    const bool k34 = k34_fused(L.tl, pl.num_passes, pl.pass_levels, G, tout);
+    int k34D = 0, k34qw = 0;
+    int64_t k34inS = 0;
     for (int i = 0; i < pl.num_passes; ++i) {
         const int D = pl.pass_levels[i];
+        if (k34 && i == pl.num_passes - 1) {  // last pass: done by k34_root_unslice (K4 below)
+            const int64_t Shi = L.Ns >> d;
+            k34D = D;
+            k34qw = int(Shi / 2);
+            k34inS = i == 0 ? in_stride0 : 2 * Shi;
+            d -= D;
+            break;
+        }
         if (kroot && i == pl.num_passes - 1) {  // D = 1 into the root
             const int64_t Shi = L.Ns >> d;
             kr.P = cur;
@@ -1948,8 +2037,28 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         rootS = outS;
     }
     // K4
-    {
-        const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
+    if (k34) {
+        const size_t sm = size_t(64 * tout + 2 * tout) * 4;
+        static std::atomic<uint32_t> k34_dev_mask{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 31 && !(k34_dev_mask.load() & (1u << dev))) {
+            cudaError_t ae = cudaSuccess;
+            ae = cudaFuncSetAttribute(k34_root_unslice<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK34SmemMax);
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(k34_root_unslice<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK34SmemMax);
+            if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(k34_root_unslice<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK34SmemMax);
+            if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
+            k34_dev_mask.fetch_or(1u << dev);
+        }
+        switch (k34D) {
+            case 1: F2X_LAUNCH(k34_root_unslice<1>, unsigned(G), kK34Threads, sm, stream, cur, C, batch, tout, k34qw, k34inS, pl.leaf_words, pl.leaf_stride, ncyc); break;
+            case 2: F2X_LAUNCH(k34_root_unslice<2>, unsigned(G), kK34Threads, sm, stream, cur, C, batch, tout, k34qw, k34inS, pl.leaf_words, pl.leaf_stride, ncyc); break;
+            case 3: F2X_LAUNCH(k34_root_unslice<3>, unsigned(G), kK34Threads, sm, stream, cur, C, batch, tout, k34qw, k34inS, pl.leaf_words, pl.leaf_stride, ncyc); break;
+            default: return F2X_ERANGE;
+        }
+    } else {
         // 32-word tiles: twice the CTAs of the slicing tiles (the grid is
         // under one wave at 64 words)
         constexpr int TW4 = 32;

@@ -473,3 +473,30 @@ def test_captured_call_replays_exactly(cuda):
         cap()
         assert np.array_equal(_np(out), ref(A[batch:], B[batch:])), (kind, size)
         assert int(cap.err_flag.item()) == 0
+
+
+@pytest.mark.parametrize("kind,size,batch", [("cyclic", 8000, 32768), ("cyclic", 4099, 40000),
+                                             ("full", 100, 32800), ("full", 64, 65536)])
+def test_k34_fused_last_pass_unslice(kind, size, batch, cuda):
+    """Karatsuba-only plans with >= 1024 groups and a last pass of <= 3
+    levels rebuild each group's root in shared memory and unslice it in the
+    same kernel (k34_root_unslice; the ring's fold by shared-memory XOR):
+    one launch fewer, bit-exact on the first/last rows and a stride
+    (ragged batches included)."""
+    from oracle import c_mul_cyclic, c_mul_full
+    from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
+    from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+
+    p = plan(kind, batch, size)
+    assert p["toom_levels"] == 0 and p["groups"] >= 1024 and p["pass_levels"][p["num_passes"] - 1] <= 3
+    assert p["launches"] == 2 + p["num_passes"], p
+    rows = np.unique(np.r_[0:40, batch - 40:batch, 0:batch:997])
+    if kind == "cyclic":
+        A, B = make_cyclic_inputs(size, batch)
+        out = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), size))
+        want = c_mul_cyclic(A[rows], B[rows], size)
+    else:
+        A, B = make_full_inputs(size, batch, words=True)
+        out = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+        want = c_mul_full(A[rows], B[rows])
+    assert np.array_equal(out[rows], want)

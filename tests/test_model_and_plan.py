@@ -395,3 +395,18 @@ def test_plan_resident_root_launches(lib):
         assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels - (1 if fused else 0), batch
     pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 35851)
     assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels
+
+
+def test_plan_k34_fusion_launches(lib):
+    """The last global pass is fused with the unslicing kernel (k34) for
+    Karatsuba-only plans with >= 1024 groups, a last pass of <= 3 levels and
+    a root stage of <= 72 KB: d-sweep d=4096 / 8192 yes, d=16384 (4 levels)
+    and the n=17669 headline (128 groups) no."""
+    from paper_2201_10473_b200 import _lib
+
+    for t, batch, fused in ((64, 1 << 20, True), (128, 1 << 19, True), (256, 1 << 18, False), (64, 4096, False)):
+        pl = _lib.make_plan(_lib.KIND_FULL, batch, t)
+        assert pl.toom_levels == 0
+        assert pl.launches == 3 + pl.num_passes - (1 if fused else 0), (t, batch)
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)
+    assert pl.launches == 3 + pl.num_passes

@@ -1,0 +1,5 @@
+# fused last pass + unslice (k34_root_unslice): parity + A/B against the separate passes
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_baseline_batches.py -q -x -k "full or dsweep or baseline or golden or forced" > gpurun_out/k34_tests.log 2>&1; echo "rc=$?" >> gpurun_out/k34_tests.log
+timeout 900 python tools/kernel_times_full.py 4096 8192 16384 > gpurun_out/k34_ab.log 2>&1
+F2X_K34=0 timeout 900 python tools/kernel_times_full.py 4096 8192 16384 >> gpurun_out/k34_ab.log 2>&1
