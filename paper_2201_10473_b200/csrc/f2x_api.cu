@@ -806,12 +806,12 @@ __host__ __device__ constexpr int kres_words(int nb, int blk) {
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
 // XORed after a barrier): no c_j round trip through HBM, one launch.
-template <int BLK, bool RES>
-__global__ void __launch_bounds__(kToomScanT, RES ? 2 : 3)
+template <int BLK, bool RES, int NT = kToomScanT>
+__global__ void __launch_bounds__(NT, RES ? 2 : (NT > 256 ? 1 : 3))
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS, const KRootIn kr) {
     extern __shared__ uint32_t tsm[];
-    constexpr int W = kToomW, ROWS = BLK / W, NSEG = kToomScanT / W, SEGR = ROWS / NSEG;
+    constexpr int W = kToomW, ROWS = BLK / W, NSEG = NT / W, SEGR = ROWS / NSEG;
     constexpr int H = BLK + 3 * W;
     const int HP = RES ? kr.hp : toom_stg_stride(BLK);  // padded stride per input (see tstg)
     uint32_t *Stg = tsm;  // [5][HP]
@@ -826,7 +826,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
     if constexpr (RES) {
         // roots -> Stg[e HP + tstg(k + 2w)], k in [-2w, nb BLK + w); zero outside [0, Lin)
         const int span = nb * BLK + 3 * W;  // resident slots h = k + 2w the block walk reads
-        for (int h = int(threadIdx.x); h < span; h += kToomScanT) {
+        for (int h = int(threadIdx.x); h < span; h += NT) {
             const int k = h - 2 * W;
             if (k < 0 || k >= Lin) {
 #pragma unroll
@@ -837,7 +837,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         const uint4 *P4 = reinterpret_cast<const uint4 *>(kr.P + item * 15 * kr.inS);
         const int64_t cs = kr.inS >> 2;  // path-product stride, quads
 #pragma unroll 1  // (2-3 items in flight per thread measured 4-16 % slower)
-        for (int x = int(threadIdx.x); x < 5 * q4; x += kToomScanT) {
+        for (int x = int(threadIdx.x); x < 5 * q4; x += NT) {
             const int e = x / q4, wq = x - e * q4;
             const uint4 *lo = P4 + (3 * e) * cs + wq, *hi = lo + cs, *mid = hi + cs;
             uint4 l[4], hh[4], m[4];
@@ -884,7 +884,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         if constexpr (RES) {
             __syncthreads();  // previous block's readers of stot / bcar are done
         } else if (vec) {  // plain, 16-byte aligned inputs: quads, all in flight per half
-            constexpr int T = kToomScanT, H4 = H / 4, NQ = (5 * H4 + T - 1) / T, NH = (NQ + 1) / 2;
+            constexpr int T = NT, H4 = H / 4, NQ = (5 * H4 + T - 1) / T, NH = (NQ + 1) / 2;
             __syncthreads();  // previous block's readers of Stg / stot are done
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -906,7 +906,7 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
                 }
             }
         } else         {  // staging: every load of the block in flight at once
-            constexpr int T = kToomScanT, NI = (H + T - 1) / T;
+            constexpr int T = NT, NI = (H + T - 1) / T;
             uint32_t v[5][NI];
             // storage offset of coefficient k = kb + tid + i T, walked
             // incrementally (one chunk split per block instead of one per
@@ -1479,6 +1479,7 @@ static int toom_seq_blk(int64_t M) {
 // product and its five roots fit in shared memory (2 CTAs/SM).
 // F2X_KROOT=0 keeps the separate k3_interp<1> pass (A/B).
 static constexpr int kResSmemMax = 110 * 1024;
+static constexpr int64_t kWideSeqMaxItems = 148;  // 512-thread form: at most one product per SM
 static bool kroot_enabled() {
     static const bool v = [] {
         const char *e = getenv("F2X_KROOT");
@@ -1994,6 +1995,10 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
                 ae = cudaFuncSetAttribute(toom_interp_seq<2304, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(5 * toom_stg_stride(2304) * 4));
             if (ae == cudaSuccess)
+                ae = cudaFuncSetAttribute(toom_interp_seq<4096, false, 512>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(5 * toom_stg_stride(4096) * 4));
+            if (ae == cudaSuccess)
                 ae = cudaFuncSetAttribute(toom_interp_seq<2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kResSmemMax);
             if (ae == cudaSuccess)
@@ -2005,7 +2010,12 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         if (seq) {
             const bool res = kroot && l == L.tl;  // roots built in shared memory from the path products
             const size_t smr = res ? size_t(5) * kr.hp * 4 : 0;
-            if (toom_seq_blk(M) == 2304) {
+            if (!res && items <= kWideSeqMaxItems && 2 * M > 4096) {
+                // at most one product per SM: 512 threads walk 4096-coefficient
+                // blocks (half the sequential block steps of the 256-thread form)
+                F2X_LAUNCH((toom_interp_seq<4096, false, 512>), unsigned(items), 512, 5 * toom_stg_stride(4096) * 4,
+                           stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS, kr);
+            } else if (toom_seq_blk(M) == 2304) {
                 if (res)
                     F2X_LAUNCH((toom_interp_seq<2304, true>), unsigned(items), kToomScanT, smr, stream, root, out, M,
                                rootLF, rootLFS, rootS, Lin, outS, kr);
