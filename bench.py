@@ -622,14 +622,40 @@ def gpu_arm(args, sync, local) -> None:
     # re-measured on another box (tools/e2e_sweep.py): copy-only ceiling 370
     # us/batch (11.06 M/s), 2 x 4 388 us, 2 x 6 389, 1 x 4 407, 1 x 6 396 --
     # the default is 2 chunks x 4 lanes
-    LANES = max(1, args.e2e_lanes)
-    hAs = [torch.from_numpy(A.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
-    hBs = [torch.from_numpy(B.view(np.int64).copy()).pin_memory() for _ in range(LANES)]
-    hCs = [torch.empty_like(hAs[0]).pin_memory() for _ in range(LANES)]
-    pipe = HostPipeline("cyclic", n, bpg, dev, chunks=args.e2e_chunks, streams=3, leaf=args.leaf,
-                        lanes=LANES)
-    graphed = all(pipe.capture(hAs[i], hBs[i], hCs[i], lane=i) for i in range(LANES)) \
-        if not args.no_graph else False
+    def make_e2e(chunks, lanes):
+        hA_ = [torch.from_numpy(A.view(np.int64).copy()).pin_memory() for _ in range(lanes)]
+        hB_ = [torch.from_numpy(B.view(np.int64).copy()).pin_memory() for _ in range(lanes)]
+        hC_ = [torch.empty_like(hA_[0]).pin_memory() for _ in range(lanes)]
+        p_ = HostPipeline("cyclic", n, bpg, dev, chunks=chunks, streams=3, leaf=args.leaf, lanes=lanes)
+        g_ = all(p_.capture(hA_[i], hB_[i], hC_[i], lane=i) for i in range(lanes)) if not args.no_graph else False
+        return p_, hA_, hB_, hC_, g_
+
+    # the pipeline shape (row chunks x lanes) is calibrated on this box before
+    # the timed region unless given: PCIe and copy-engine behaviour vary
+    # between boxes of the pool (tools/e2e_sweep.py: the best shape was 2 x 4
+    # on one box, 1 x 4 on another where concurrent H2D+D2H ran at 51 GB/s)
+    calib = {}
+    if args.e2e_chunks > 0:
+        CHUNKS, LANES = args.e2e_chunks, max(1, args.e2e_lanes)
+    else:
+        for ch, ln in ((1, 2), (1, 4), (2, 2), (2, 4), (4, 4)):
+            p_, hA_, hB_, hC_, _ = make_e2e(ch, ln)
+            for j in range(2 * ln):
+                p_.run(hA_[j % ln], hB_[j % ln], hC_[j % ln], lane=j % ln)
+            p_.join()
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            for j in range(24):
+                p_.run(hA_[j % ln], hB_[j % ln], hC_[j % ln], lane=j % ln)
+            p_.join()
+            c1.record()
+            torch.cuda.synchronize()
+            calib[f"{ch}x{ln}"] = round(c0.elapsed_time(c1) / 24, 4)
+            del p_, hA_, hB_, hC_
+        best = min(calib, key=calib.get)
+        CHUNKS, LANES = (int(x) for x in best.split("x"))
+    pipe, hAs, hBs, hCs, graphed = make_e2e(CHUNKS, LANES)
     e2e_i = [0]
 
     def e2e_step():
@@ -756,11 +782,13 @@ def gpu_arm(args, sync, local) -> None:
                 "ms_per_step": round(e2e_ms, 5),
                 "parity_ok": bool(bad_e2e == 0.0),
                 "path": f"pinned host A,B -> H2D -> mul_cyclic (C ABI) -> D2H; engine.HostPipeline, "
-                        f"{args.e2e_chunks} row chunk(s) per batch"
+                        f"{CHUNKS} row chunk(s) per batch"
                         + (", each batch replayed as one CUDA graph" if graphed else ", eager launches")
                         + f"; {LANES} host batches in flight (one pinned buffer set per lane), so a "
                         "batch's copies overlap the previous batches' kernels; pipeline fill and "
                         "drain inside the timed region",
+                "pipeline_shape": f"{CHUNKS}x{LANES}",
+                "calibration_ms_per_batch": calib or None,
             },
             "plan_work": {
                 "leaf_lop3_per_product": round(pl["leaf_ops_per_product"], 1),
@@ -770,7 +798,7 @@ def gpu_arm(args, sync, local) -> None:
             },
             "ncu_node_kernel": committed_ncu(pl),
             "paper_avx512_1core_products_s": round(PAPER_1CORE[N_RING], 1) if n == N_RING else None,
-            "gpu_launches": int(2 * K * pl["launches"]),
+            "gpu_launches": int((K + max(3, K // 2) * CHUNKS) * pl["launches"]),
             "clocks": cl,
         }
         if scaling:
@@ -862,11 +890,13 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=N_RING)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
     ap.add_argument("--leaf", type=int, default=0)
-    ap.add_argument("--e2e-chunks", type=int, default=2,
-                    help="row chunks per host batch in the e2e pipeline")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="row chunks per host batch in the e2e pipeline (0: calibrate chunks x lanes "
+                         "on this box before the timed region)")
     ap.add_argument("--no-graph", action="store_true", help="eager e2e launches (no CUDA graph)")
     ap.add_argument("--e2e-lanes", type=int, default=4,
-                    help="host batches in flight in the e2e pipeline (one pinned buffer set each)")
+                    help="host batches in flight in the e2e pipeline (one pinned buffer set each; with "
+                         "--e2e-chunks > 0)")
     ap.add_argument("--quick", action="store_true", help="headline only (no per-config / scaling lines)")
     ap.add_argument("--no-dsweep", action="store_true", help="skip the configs[4] d-sweep lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
