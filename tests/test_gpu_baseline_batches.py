@@ -137,7 +137,7 @@ def test_bench_two_ranks_spawned_functional(cuda):
     env = dict(os.environ, NCCL_DEBUG="INFO")
     env.pop("WORLD_SIZE", None)
     r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--share-device", "--steps", "5", "--warmup",
-                        "3", "--no-cpu", "--no-dsweep", "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env,
+                        "3", "--no-cpu", "--no-dsweep", "--e2e-chunks", "1", "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -167,7 +167,7 @@ def test_bench_two_ranks_torchrun_functional(cuda):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
                         "--share-device", "--steps", "5", "--warmup", "3", "--no-cpu", "--no-dsweep",
-                        "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env, capture_output=True, text=True,
+                        "--e2e-chunks", "1", "--e2e-lanes", "1", "--batch", "1024"], cwd=root, env=env, capture_output=True, text=True,
                        timeout=1200)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
