@@ -108,6 +108,13 @@ for n, b in ((12323, 256), (17669, 96), (35851, 64), (57637, 40)):
 for t, b in ((16, 33), (128, 9), (512, 5), (1024, 3), (4096, 2)):
     A, B = make_full_inputs(t, b, words=True)
     assert np.array_equal(mul_full(d(A), d(B)).cpu().numpy().view(np.uint64), c_mul_full(A, B)), t
+# >= 1024 groups: the fused last-pass + unslicing kernel (k34_root_unslice) when no Toom level is forced
+rows = np.r_[0:40, 32728:32768]
+A, B = make_full_inputs(64, 32768, words=True)
+assert np.array_equal(mul_full(d(A), d(B)).cpu().numpy().view(np.uint64)[rows], c_mul_full(A[rows], B[rows]))
+A, B = make_cyclic_inputs(8000, 32768)
+assert np.array_equal(mul_cyclic(d(A), d(B), 8000).cpu().numpy().view(np.uint64)[rows],
+                      c_mul_cyclic(A[rows], B[rows], 8000))
 print("ok", plan("cyclic", 40, 57637)["toom_levels"])
 """
 
