@@ -1023,24 +1023,15 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
         }
         __syncthreads();
         // ... second contributions XOR onto them (written by this CTA, earlier
-        // or before the barrier above); loads of a half batch first
-        constexpr int HB = (SEGR + 1) / 2;  // rows per half batch (SEGR may be odd)
+        // or before the barrier above) as fire-and-forget L2 reductions
+        // (red.global.xor: no load round trip; XOR commutes, and the barrier
+        // orders every first contribution before them)
 #pragma unroll
-        for (int h2 = 0; h2 < SEGR; h2 += HB) {
-            uint32_t old[HB][4];
+        for (int i = 0; i < SEGR; ++i) {
+            const int k = kr0 + i * W;
+            if (k < L && k >= M) {
 #pragma unroll
-            for (int i = 0; i < HB; ++i) {
-                const int k = kr0 + (h2 + i) * W;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) old[i][j] = (h2 + i < SEGR && k < L && k >= M) ? Rg[k + j * M] : 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < HB; ++i) {
-                const int k = kr0 + (h2 + i) * W;
-                if (h2 + i < SEGR && k < L && k >= M) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) Rg[k + j * M] = old[i][j] ^ keep[h2 + i][j];
-                }
+                for (int j = 0; j < 4; ++j) atomicXor(Rg + k + j * M, keep[i][j]);
             }
         }
         if (sg == NSEG - 1) {  // carry into the next block: this block's chain totals
