@@ -1021,10 +1021,12 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
                 c4m1 = c4;
             }
         }
-        __syncthreads();
+        // a second contribution's first one comes from coefficient k - M: from
+        // this block only when M < BLK (then a barrier orders the two)
+        if (M < BLK) __syncthreads();
         // ... second contributions XOR onto them (written by this CTA, earlier
         // or before the barrier above) as fire-and-forget L2 reductions
-        // (red.global.xor: no load round trip; XOR commutes, and the barrier
+        // (red.global.xor: no load round trip; XOR commutes, and a barrier
         // orders every first contribution before them)
 #pragma unroll
         for (int i = 0; i < SEGR; ++i) {
