@@ -858,19 +858,18 @@ toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int 
             }
             const int c = wq / qsz, r0 = 4 * (wq - c * qsz);  // chunk, first word in it
             const int kq = c * kr.LF + r0 + 2 * W;             // resident index of octant 0's first word
-            uint32_t *S0 = Stg + e * HP;
-            const int nw = min(4, kr.LF - r0);  // data words in this storage quad
+            const int base = e * HP, dump = base + HP - 1;  // (a spare slot past the walk's span)
+            const int nw = min(4, kr.LF - r0);             // data words in this storage quad
 #pragma unroll
             for (int mo = 0; mo < 8; ++mo) {
                 const uint32_t vv[4] = {o[mo].x, o[mo].y, o[mo].z, o[mo].w};
                 // one tstg per quad: the four words are consecutive slots unless
-                // they cross a 128-word pad boundary (then +16 from there on)
+                // they cross a 128-word pad boundary (then +16 from there on);
+                // a chunk's pad word goes to the spare slot (no branches)
                 const int h0 = kq + mo * kr.oc;
-                uint32_t *d0 = S0 + tstg(h0);
-                const int cross = 128 - (h0 & 127);  // first j past the boundary
+                const int t0 = base + tstg(h0), cross = 128 - (h0 & 127);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (j < nw) d0[j + (j >= cross ? 16 : 0)] = vv[j];
+                for (int j = 0; j < 4; ++j) Stg[j < nw ? t0 + j + (j >= cross ? 16 : 0) : dump] = vv[j];
             }
         }
         __syncthreads();
