@@ -797,7 +797,8 @@ struct KRootIn {
     int qw, oc, LF, LFS;
     int hp;  // resident root stride in shared memory, words
 };
-// resident root index of coefficient k (k >= -2w): tstg layout, 2w halo
+// words per resident root: slots h = k + 2w for k in [-2w, nb blk + w) in the
+// tstg layout, plus a spare slot past the walk's span (branch-free stores)
 __host__ __device__ constexpr int kres_words(int nb, int blk) {
     return (nb * blk + 3 * kToomW) + 16 * (((nb * blk + 3 * kToomW) >> 7) + 1);
 }
@@ -805,7 +806,8 @@ __host__ __device__ constexpr int kres_words(int nb, int blk) {
 // Single-kernel variant: one CTA per item walks its blocks in order, so the
 // chain carries flow from block to block in shared memory and the c_j go
 // straight into R (first contribution to a coefficient written, the second
-// XORed after a barrier): no c_j round trip through HBM, one launch.
+// added by an L2 XOR reduction): no c_j round trip through HBM, one launch.
+// NT = 512 (with BLK = 4096) for levels with at most one product per SM.
 template <int BLK, bool RES, int NT = kToomScanT>
 __global__ void __launch_bounds__(NT, RES ? 2 : (NT > 256 ? 1 : 3))
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
