@@ -1644,8 +1644,14 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.off_p0 = align256(L.off_bbs + opw * 4);
     const int64_t p0 = G2 * ipow3(GL) * 2 * L.Ss * 4;  // node products
     L.off_p1 = align256(L.off_p0 + p0);
+    // the last pass is folded into a later kernel (resident-root Toom
+    // interpolation or k34_root_unslice): it writes nothing to the ping-pong
+    // buffers
+    const int tout_pl = kind == F2X_KIND_FULL ? 2 * t : t;
+    const int np_exec = np - ((kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ||
+                               k34_fused(TL, np, pl->pass_levels, G, tout_pl)) ? 1 : 0);
     int64_t p1 = 0;
-    if (np >= 1) {  // first pass output (the largest one written to P1)
+    if (np_exec >= 1) {  // first pass output (the largest one written to P1)
         const int d1 = GL - pl->pass_levels[0];
         p1 = G2 * ipow3(d1) * 2 * (L.Ns >> d1) * 4;
     }
@@ -1664,7 +1670,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     L.total = off;
     {  // every pass output must fit the ping-pong buffer it is written to
         int d = GL;
-        for (int i = 0; i < np; ++i) {
+        for (int i = 0; i < np_exec; ++i) {
             const int dlo = d - pl->pass_levels[i];
             const int64_t outb = G2 * ipow3(dlo) * 2 * (L.Ns >> dlo) * 4;
             if (outb > ((i & 1) ? p0 : p1)) return F2X_ERANGE;

@@ -410,3 +410,18 @@ def test_plan_k34_fusion_launches(lib):
         assert pl.launches == 3 + pl.num_passes - (1 if fused else 0), (t, batch)
     pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)
     assert pl.launches == 3 + pl.num_passes
+
+
+def test_plan_fused_last_pass_needs_no_pingpong_buffer(lib):
+    """When the only global pass is folded into a later kernel (resident-root
+    interpolation at n=57637, k34 at d=4096) the plan does not reserve the
+    pass's output buffer: F2X_KROOT / F2X_K34 are read once per process, so
+    compare against the closed-form size of that buffer instead."""
+    from paper_2201_10473_b200 import _lib
+
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 16384, 57637)
+    assert pl.num_passes == 1 and pl.launches == 2 + pl.num_passes + 2 * pl.toom_levels
+    assert pl.workspace_bytes < 4.5 * 2 ** 30  # 5.27 GiB with the pass output buffer
+    pl = _lib.make_plan(_lib.KIND_FULL, 1 << 20, 64)
+    assert pl.num_passes == 1 and pl.launches == 2 + pl.num_passes
+    assert pl.workspace_bytes < 5.5 * 2 ** 30  # 6.19 GiB with it
