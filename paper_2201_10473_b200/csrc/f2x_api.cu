@@ -425,6 +425,39 @@ __device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, 
     }
 }
 
+// eval_l1_point with the point E a runtime (CTA-uniform) value: one code
+// copy for all five points, so the point loop below stays a loop without an
+// indirect-branch dispatch (tools/ct_sass_audit.py) and without the spills
+// of a written-out sequence.  Unused terms load nothing and are zero.
+__device__ __forceinline__ void eval_l1_point_rt(int E, const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo,
+                                                 int k0, int nq1, int tid) {
+    constexpr int w = kToomW, wq = kToomW / 4, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
+    const int M2 = geo.M[2], M3 = geo.M[3], M1 = geo.M[1];
+    const bool use_a0 = E <= 3, use_a1 = E == 1 || E == 3, use_a2 = E == 1 || E == 3 || E == 4,
+               use_s = E == 2 || E == 3;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int pi1 = 0; pi1 < 9; ++pi1) {
+        const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
+        const int sig1 = p2 * M2 + p3 * M3 + k0 - 4 * w;
+        const uint4 *P0 = reinterpret_cast<const uint4 *>(L0 + pi1 * Z0);
+        const uint4 *P1 = reinterpret_cast<const uint4 *>(L0 + (9 + pi1) * Z0);
+        const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
+        uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
+        for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
+            const int k = sig1 + 4 * jq;
+            const bool ka = unsigned(k) < unsigned(M1), k1 = unsigned(k - w) < unsigned(M1),
+                       k2 = unsigned(k - 2 * w) < unsigned(M1);
+            const uint4 a0 = (use_a0 && ka) ? P0[jq + 2 * wq] : z;
+            const uint4 a1 = (use_a1 && ka) ? P1[jq + 2 * wq] : z;
+            const uint4 a2 = (use_a2 && ka) ? P2[jq + 2 * wq] : z;
+            const uint4 s1 = (use_s && k1) ? P1[jq + wq] : z;
+            const uint4 s2 = (use_s && k2) ? P2[jq] : z;
+            D[jq] = xor3(a0, a1, a2) ^ (s1 ^ s2);
+        }
+    }
+}
+
 // all five points of nq quads of `np` pieces at once: piece p of the output
 // (of every point e) from input pieces (0, p), (1, p), (2, p) (stride np);
 // output piece (e, p) at D + (e np + p) Zd
@@ -613,17 +646,21 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
         for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
         const int M2 = geo.M[2];
 #pragma unroll
+        // phases: L1(0) | L2(0) | final(0) + L1(1) | L2(1) | ... | final(4):
+        // the next point's level-1 pass writes only L1, which the final level
+        // does not read, so it shares the final level's phase (11 phases
+        // instead of 15 for the same barriers)
+        eval_l1_point_rt(0, L0, L1, geo, k0, nq1, tid);
+        __syncthreads();
+#pragma unroll 1
         for (int e1 = 0; e1 < 5; ++e1) {
-            if (e1 == 0) eval_l1_point<0>(L0, L1, geo, k0, nq1, tid);
-            if (e1 == 1) eval_l1_point<1>(L0, L1, geo, k0, nq1, tid);
-            if (e1 == 2) eval_l1_point<2>(L0, L1, geo, k0, nq1, tid);
-            if (e1 == 3) eval_l1_point<3>(L0, L1, geo, k0, nq1, tid);
-            if (e1 == 4) eval_l1_point<4>(L0, L1, geo, k0, nq1, tid);
-            __syncthreads();
             eval_level5(L1, Z1, L2, Z2, 3, nq2, sig2, M2, tid);
             __syncthreads();
             final_level(L2, Z2, g * 5 + e1);
-            // (the next level-1 pass writes only L1; L2 is rewritten after its barrier)
+            if (e1 < 4) {
+                eval_l1_point_rt(e1 + 1, L0, L1, geo, k0, nq1, tid);
+                __syncthreads();
+            }
         }
     }
 }
