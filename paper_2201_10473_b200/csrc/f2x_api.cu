@@ -400,32 +400,8 @@ __device__ __forceinline__ void eval_quad(const uint4 *P0, const uint4 *P1, cons
     }
 }
 
-// level-1 pieces (9 of them) of one evaluation point E from the 27 level-0
-// pieces (TL = 3); E is a compile-time constant (the e1 loop is unrolled:
-// each point reads only the pieces it needs, and there is no indirect branch
-// -- tools/ct_sass_audit.py)
-template <int E>
-__device__ __forceinline__ void eval_l1_point(const uint32_t *L0, uint32_t *L1, const ToomEvalGeo &geo, int k0,
-                                              int nq1, int tid) {
-    constexpr int w = kToomW, Z0 = efslot(3, 0), Z1 = efslot(3, 1);
-    const int M2 = geo.M[2], M3 = geo.M[3], M1 = geo.M[1];
-#pragma unroll
-    for (int pi1 = 0; pi1 < 9; ++pi1) {
-        const int p2 = pi1 / 3, p3 = pi1 - 3 * p2;
-        const int sig1 = p2 * M2 + p3 * M3 + k0 - 4 * w;
-        const uint4 *P0 = reinterpret_cast<const uint4 *>(L0 + pi1 * Z0);
-        const uint4 *P1 = reinterpret_cast<const uint4 *>(L0 + (9 + pi1) * Z0);
-        const uint4 *P2 = reinterpret_cast<const uint4 *>(L0 + (18 + pi1) * Z0);
-        uint4 *D = reinterpret_cast<uint4 *>(L1 + pi1 * Z1);
-        for (int jq = tid; jq < nq1; jq += kEvalFusedThreads) {
-            uint4 y[1];
-            eval_quad<E>(P0, P1, P2, jq, sig1 + 4 * jq, M1, y);
-            D[jq] = y[0];
-        }
-    }
-}
-
-// eval_l1_point with the point E a runtime (CTA-uniform) value: one code
+// Level-1 pieces (9 of them) of evaluation point E from the 27 level-0
+// pieces (TL = 3), with the point E a runtime (CTA-uniform) value: one code
 // copy for all five points, so the point loop below stays a loop without an
 // indirect-branch dispatch (tools/ct_sass_audit.py) and without the spills
 // of a written-out sequence.  Unused terms load nothing and are zero.
