@@ -500,3 +500,18 @@ def test_k34_fused_last_pass_unslice(kind, size, batch, cuda):
         out = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
         want = c_mul_full(A[rows], B[rows])
     assert np.array_equal(out[rows], want)
+
+
+def test_release_workspaces_gpu(cuda):
+    """The per-stream scratch cache refills after engine.release_workspaces
+    and products stay exact."""
+    from oracle import c_mul_cyclic
+    from oracle.f2x_oracle import make_cyclic_inputs
+    from paper_2201_10473_b200 import engine, mul_cyclic
+
+    A, B = make_cyclic_inputs(17669, 64)
+    want = c_mul_cyclic(A, B, 17669)
+    assert np.array_equal(_np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), 17669)), want)
+    assert engine.release_workspaces(cuda.index) > 0 and not any(k[0] == cuda.index for k in engine._workspaces)
+    assert np.array_equal(_np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), 17669)), want)
+    assert any(k[0] == cuda.index for k in engine._workspaces)
