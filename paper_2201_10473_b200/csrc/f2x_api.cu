@@ -621,7 +621,6 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
 #pragma unroll
         for (int p = 0; p < 3; ++p) sig2[p] = p * geo.M[3] + k0 - 2 * w;
         const int M2 = geo.M[2];
-#pragma unroll
         // phases: L1(0) | L2(0) | final(0) + L1(1) | L2(1) | ... | final(4):
         // the next point's level-1 pass writes only L1, which the final level
         // does not read, so it shares the final level's phase (11 phases
