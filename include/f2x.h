@@ -88,6 +88,12 @@ typedef struct f2x_plan {
 F2X_API int f2x_make_plan(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint,
                   f2x_plan *plan);
 
+/* Planner cost model (tests / tuning): modelled cost per 32-product group,
+ * in leaf-LOP3 units, of the best plan with toom_levels Toom-3 levels for
+ * this call shape; < 0 if no such plan exists.  f2x_make_plan takes the
+ * cheapest level count among those it considers for the shape. */
+F2X_API double f2x_plan_cost(int32_t kind, int64_t batch, int32_t t_or_n, int32_t toom_levels);
+
 /* Workspace bytes for f2x_mul_full(batch, t) / f2x_mul_cyclic(batch, n). */
 F2X_API int64_t f2x_workspace_bytes(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint);
 

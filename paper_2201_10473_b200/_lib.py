@@ -30,6 +30,7 @@ KIND_CYCLIC = 1
 
 EXPORTS = (
     "f2x_make_plan",
+    "f2x_plan_cost",
     "f2x_workspace_bytes",
     "f2x_mul_full",
     "f2x_mul_cyclic",
@@ -98,6 +99,8 @@ def load() -> ctypes.CDLL:
         vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
         lib.f2x_make_plan.argtypes = [i32, i64, i32, i32, ctypes.POINTER(F2xPlan)]
         lib.f2x_make_plan.restype = ctypes.c_int
+        lib.f2x_plan_cost.argtypes = [i32, i64, i32, i32]
+        lib.f2x_plan_cost.restype = ctypes.c_double
         lib.f2x_workspace_bytes.argtypes = [i32, i64, i32, i32]
         lib.f2x_workspace_bytes.restype = i64
         lib.f2x_mul_full.argtypes = [vp, vp, vp, i64, i32, vp, sz, i32, vp]

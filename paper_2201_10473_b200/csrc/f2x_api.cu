@@ -48,7 +48,14 @@ static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
 static constexpr int kToomW = 16;       // x = X^w (coefficients)
 static constexpr double kToomWordCost = 15.0;  // planner: cost units per word moved (fit on B200)
-static constexpr int kToomMinWords = 512;      // Toom from 512 words: d=32768 (t=512) 27.26 -> 25.79 ms with two levels (round 2); t=256 slower (17.90 vs 18.76 ms)
+static constexpr int kToomMinWords = 512;      // Toom at any batch from 512 words: d=32768 (t=512) 27.26 -> 25.79 ms with two levels (round 2)
+// Below 512 words Toom pays only when its passes fill the GPU (measured, us per
+// call, TL 0/1/2: n=17669 x 2048 167/201/177 but x 4096 324/365/311 and x 16384
+// 1260/1422/1171; n=20000 x 4096 456/432/358; n=12323 x 4096 213/201/218; n=10000
+// 161/162/164; n=8000 108/128/118): considered from 160 words and 128 groups.
+static constexpr int kToomMinWordsBatched = 160;
+static constexpr int64_t kToomMinGroupsBatched = 128;
+static constexpr double kPassWordCost = 16.0;  // planner: global Karatsuba passes / slicing output, per word (n=17669 k3_interp<4>: 18.9 us for 128 x 223.5 K words)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -1547,6 +1554,68 @@ static int toom_leaf_override() {
     return v;
 }
 
+// Words moved per node-problem group by the memory passes around the node
+// kernel of a (TL, LF, K) plan: the pre-evaluated operand slices written by
+// k1_slice_eval (Karatsuba-only plans) and every global interpolation pass
+// (children read + parent written; a last pass folded into the resident-root
+// Toom interpolation or into k34_root_unslice costs only the children's extra
+// words over the parent's).
+static double karatsuba_pass_words(int kind, int t, int TL, int LF, int K, int64_t G, const int64_t *M) {
+    const int KC = std::min(K, kMaxKC), GL = K - KC;
+    const int64_t LFS = leaf_stride_words(LF), Ns = LFS << K, Ss = LFS << KC;
+    double w = 0;
+    if (TL == 0) {
+        const int el = eval_levels_for(GL, int64_t(LF) << K);
+        w += 2.0 * double(ipow3(el)) * double(Ns >> el);
+    }
+    int32_t pass_levels[kMaxGL] = {0};
+    int rem = GL, np = 0;
+    while (rem > 0) {
+        const int p = std::min(kMaxPassLevels, rem);
+        pass_levels[np++] = p;
+        rem -= p;
+    }
+    const bool folded = np > 0 && (kroot_fused(TL, np, pass_levels, G, M[TL]) ||
+                                   k34_fused(TL, np, pass_levels, G, kind == F2X_KIND_FULL ? 2 * t : t));
+    rem = GL;
+    int64_t S = 2 * Ss;  // words of one product at the current level
+    for (int i = 0; i < np; ++i) {
+        w += double(ipow3(rem)) * double(S);
+        rem -= pass_levels[i];
+        S <<= pass_levels[i];
+        // a folded pass writes no parent, and its consumer reads the children
+        // instead of the parent it is already charged for
+        w += (folded && i == np - 1 ? -1.0 : 1.0) * double(ipow3(rem)) * double(S);
+    }
+    return w;
+}
+
+static bool toom_considered(int t, int64_t G) {
+    return t >= kToomMinWords || (t >= kToomMinWordsBatched && G >= kToomMinGroupsBatched);
+}
+
+// Modelled cost per 32-product group of the best (LF, K) under TL Toom-3
+// levels (cost units: ~one leaf LOP3 per group): node kernel (best_leaf), the
+// global Karatsuba passes and slicing output, and the Toom passes.
+static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, int &LF, int &K, int64_t *M,
+                           double &c) {
+    const int64_t Nmin = int64_t(64) * t;
+    int64_t Smin = Nmin;
+    if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
+    if (!best_leaf(Smin, TL > 0 && toom_leaf_override() ? toom_leaf_override() : leaf_hint, LF, K, c)) return false;
+    c += kPassWordCost * karatsuba_pass_words(kind, t, TL, LF, K, G, M);
+    c *= double(ipow5(TL));
+    if (TL > 0) c += kPassWordCost * 2.0 * 3.0 * double(M[1]);  // plain bitsliced slice (k1_slice)
+    // Toom passes are HBM-bound: ~kToomWordCost per word moved per group
+    for (int l = 1; l <= TL; ++l) {
+        const double Sl = l < TL ? 3.0 * double(M[l + 1]) : double(int64_t(LF) << K);
+        const double ev = 2.0 * double(ipow5(l - 1)) * 3.0 * double(M[l]) + 2.0 * double(ipow5(l)) * Sl;
+        const double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
+        c += kToomWordCost * (ev + ip);
+    }
+    return true;
+}
+
 static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
                      Layout *lay) {
     if (!pl || batch < 1 || t_or_n < 1) return F2X_EINVAL;
@@ -1568,22 +1637,14 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     double best = 0;
     int64_t bestM[kMaxToom + 1] = {0};
     const int forced = leaf_hint ? 0 : toom_override();
+    const int64_t Gp = ceil_div(batch, 32);
     for (int TL = 0; TL <= kMaxToom; ++TL) {
         if (forced >= 0 && TL != forced) continue;
-        if (TL > 0 && (leaf_hint || (forced < 0 && t < kToomMinWords))) continue;
-        int64_t M[kMaxToom + 1] = {0}, Smin = Nmin;
-        if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
+        if (TL > 0 && (leaf_hint || (forced < 0 && !toom_considered(t, Gp)))) continue;
+        int64_t M[kMaxToom + 1] = {0};
         int LF, K;
         double c;
-        if (!best_leaf(Smin, TL > 0 && toom_leaf_override() ? toom_leaf_override() : leaf_hint, LF, K, c)) continue;
-        c *= double(ipow5(TL));
-        // Toom passes are HBM-bound: ~kToomWordCost per word moved per group
-        for (int l = 1; l <= TL; ++l) {
-            const double Sl = l < TL ? 3.0 * double(M[l + 1]) : double(int64_t(LF) << K);
-            const double ev = 2.0 * double(ipow5(l - 1)) * 3.0 * double(M[l]) + 2.0 * double(ipow5(l)) * Sl;
-            const double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
-            c += kToomWordCost * (ev + ip);
-        }
+        if (!plan_candidate(kind, t, TL, leaf_hint, Gp, LF, K, M, c)) continue;
         if (bestTL < 0 || c < best) {
             best = c;
             bestTL = TL;
@@ -2123,6 +2184,18 @@ extern "C" {
 int f2x_make_plan(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint,
                   f2x_plan *plan) {
     return f2x::plan_impl(kind, batch, t_or_n, leaf_hint, plan, nullptr);
+}
+
+double f2x_plan_cost(int32_t kind, int64_t batch, int32_t t_or_n, int32_t toom_levels) {
+    if ((kind != F2X_KIND_FULL && kind != F2X_KIND_CYCLIC) || batch < 1 || t_or_n < 1 || toom_levels < 0 ||
+        toom_levels > f2x::kMaxToom)
+        return -1.0;
+    const int t = kind == F2X_KIND_FULL ? t_or_n : (t_or_n + 63) / 64;
+    int64_t M[f2x::kMaxToom + 1] = {0};
+    int LF, K;
+    double c;
+    if (!f2x::plan_candidate(kind, t, toom_levels, 0, f2x::ceil_div(batch, 32), LF, K, M, c)) return -1.0;
+    return c;
 }
 
 int64_t f2x_workspace_bytes(int32_t kind, int64_t batch, int32_t t_or_n, int32_t leaf_hint) {

@@ -110,13 +110,45 @@ def test_plan_struct_size_matches_header(lib):
     """ctypes mirror of f2x_plan must have the C layout (field offsets)."""
     from paper_2201_10473_b200 import _lib
 
-    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)
-    assert pl.t == 277 and pl.n == 17669 and pl.groups == 128
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 2048, 17669)  # 64 groups: Karatsuba only
+    assert pl.t == 277 and pl.n == 17669 and pl.groups == 64 and pl.toom_levels == 0
     assert pl.N >= 64 * 277 and pl.N == pl.leaf_words << pl.levels
     assert pl.levels == pl.cta_levels + pl.global_levels
     assert sum(pl.pass_levels[: pl.num_passes]) == pl.global_levels
     assert pl.launches == 3 + pl.num_passes
     assert pl.workspace_bytes > 0
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)  # 128 groups: two Toom-3 levels
+    assert pl.t == 277 and pl.groups == 128 and pl.toom_levels == 2 and pl.toom_w == 16
+    assert pl.N == 3 * pl.toom_M[0] >= 64 * 277
+    assert pl.leaf_words << pl.levels >= pl.toom_M[1] + 2 * pl.toom_w
+    assert pl.node_ctas == 128 * 25 * 3 ** pl.global_levels
+    # one global level, folded into the resident-root interpolation
+    assert pl.global_levels == 1 and pl.launches == 3 + 1 + 2 * 2 - 1
+
+
+# (kind, batch, t_or_n) -> Toom-3 levels measured fastest on B200 (DESIGN §7b
+# "planner regret"; tools/runs/toomgrid2.sh): the picks below 512 words need
+# 128 groups to fill the GPU with the Toom passes
+PLANNER_PINS = [
+    (1, 256, 12323, 0), (1, 4096, 12323, 1), (1, 2048, 17669, 0), (1, 4096, 17669, 2),
+    (1, 16384, 17669, 2), (1, 4096, 9000, 0), (1, 4096, 14000, 2), (1, 4096, 20000, 2),
+    (1, 4096, 24000, 1), (1, 4096, 28000, 3), (1, 4096, 32000, 2), (1, 4096, 35851, 2),
+    (1, 16384, 57637, 3), (0, 1 << 20, 64, 0), (0, 1 << 19, 128, 0), (0, 1 << 18, 256, 0),
+    (0, 1 << 17, 512, 2), (0, 1 << 16, 1024, 2),
+]
+
+
+@pytest.mark.parametrize("kind,batch,size,tl", PLANNER_PINS)
+def test_planner_toom_depth_pins(lib, kind, batch, size, tl):
+    from paper_2201_10473_b200 import _lib
+
+    pl = _lib.make_plan(kind, batch, size)
+    assert pl.toom_levels == tl
+    # the pick is the cheapest modelled depth among those considered
+    costs = [lib.f2x_plan_cost(kind, batch, size, k) for k in range(4)]
+    assert all(c > 0 for c in costs)
+    assert costs[tl] == min(costs) or tl == 0
+    assert lib.f2x_plan_cost(kind, batch, size, 4) < 0 and lib.f2x_plan_cost(5, batch, size, 0) < 0
 
 
 @pytest.mark.parametrize("t", list(range(1, 70)) + [100, 128, 193, 256, 277, 512, 561, 901, 1024, 2048])
@@ -401,15 +433,15 @@ def test_plan_k34_fusion_launches(lib):
     """The last global pass is fused with the unslicing kernel (k34) for
     Karatsuba-only plans with >= 1024 groups, a last pass of <= 3 levels and
     a root stage of <= 72 KB: d-sweep d=4096 / 8192 yes, d=16384 (4 levels)
-    and the n=17669 headline (128 groups) no."""
+    and n=17669 x 2048 (64 groups) no."""
     from paper_2201_10473_b200 import _lib
 
     for t, batch, fused in ((64, 1 << 20, True), (128, 1 << 19, True), (256, 1 << 18, False), (64, 4096, False)):
         pl = _lib.make_plan(_lib.KIND_FULL, batch, t)
         assert pl.toom_levels == 0
         assert pl.launches == 3 + pl.num_passes - (1 if fused else 0), (t, batch)
-    pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)
-    assert pl.launches == 3 + pl.num_passes
+    pl = _lib.make_plan(_lib.KIND_CYCLIC, 2048, 17669)
+    assert pl.toom_levels == 0 and pl.launches == 3 + pl.num_passes
 
 
 def test_plan_fused_last_pass_needs_no_pingpong_buffer(lib):
