@@ -87,8 +87,12 @@ def committed_ncu(pl) -> dict | None:
             d = dict(zip(rows[0], rows[2]))
             dur_s = float(d["gpu__time_duration.sum"]) * 1e-6
             dram = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * 1e6
+            name = f"k2_node_mul<{pl['leaf_words']}, {pl['cta_levels']}>"
+            if name not in d["Kernel Name"] or f"({pl['node_ctas']}," not in d["Grid Size"]:
+                continue
             out = {
                 "source": os.path.relpath(f, ROOT),
+                "kernel": name, "grid": int(pl["node_ctas"]),
                 "pipe_alu_pct": float(d["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"]),
                 "pipe_fma_pct": float(d["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"]),
                 "issue_active_pct": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
@@ -97,7 +101,7 @@ def committed_ncu(pl) -> dict | None:
             }
         except Exception:
             continue
-    return out if pl.get("leaf_words") == 35 else None
+    return out
 
 
 def committed_traffic(pl) -> dict | None:
@@ -111,14 +115,16 @@ def committed_traffic(pl) -> dict | None:
             d = json.load(open(f))
         except Exception:
             continue
-        if d.get("workload") == "n=17669 x4096" and pl.get("leaf_words") == 35:
-            # algorithmic: both (pre-evaluated) bitsliced operands read once + every
-            # node product written once
+        if (d.get("workload") == "n=17669 x4096" and
+                d.get("kernel") == f"k2_node_mul<{pl['leaf_words']},{pl['cta_levels']}>" and
+                d.get("grid", pl["node_ctas"]) == pl["node_ctas"]):
+            # algorithmic: both (pre-evaluated) bitsliced node-problem operands read
+            # once + every node product written once
             el = pl.get("eval_levels", 0)
             ns = 3 ** el * (pl["leaf_stride"] << (pl["levels"] - el))
             ss = pl["leaf_stride"] << pl["cta_levels"]
             words = 3 ** pl["global_levels"] * 2 * ss
-            alg = 4 * pl["groups"] * (2 * ns + words)
+            alg = 4 * pl["groups"] * 5 ** pl.get("toom_levels", 0) * (2 * ns + words)
             best = {"dram_bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"],
                     "algorithmic_bytes_per_launch": alg,
                     "note": "DRAM < algorithmic: L2 (126 MB) absorbs most node-product writes"}
@@ -720,8 +726,13 @@ def gpu_arm(args, sync, local) -> None:
 
     if rank == 0:
         W = w_alg(t)
+        # the node kernel's units: 5^TL node problems of LF 2^K coefficients per
+        # product under TL Toom-3 levels (the whole product when TL = 0)
+        TL = int(pl.get("toom_levels", 0))
+        t_node = (pl["leaf_words"] << pl["levels"]) / 64.0
+        W_node = 5 ** TL * w_alg(t_node, cyclic=False) if TL else W
         node_s = node_ms / K / 1e3
-        achieved = bpg * W / node_s / 1e12
+        achieved = bpg * W_node / node_s / 1e12
         pk = peak["ops_per_s"] / 1e12
         cl = clk.summary()
         nominal = peak["sms"] * 64 * (cl["sm_max_mhz"] or 1965) * 1e6 / 1e12
@@ -749,7 +760,8 @@ def gpu_arm(args, sync, local) -> None:
                 "step": "engine.CapturedCall: the call's launches captured once as a CUDA graph and "
                         "replayed per step (eager per-step time in roofline.eager_ms_per_step)",
                 "plan": {k: pl[k] for k in ("N", "leaf_words", "levels", "cta_levels",
-                                             "global_levels", "pass_levels", "eval_levels", "node_ctas")},
+                                             "global_levels", "pass_levels", "eval_levels", "node_ctas",
+                                             "toom_levels", "toom_M", "launches")},
             },
             "parity": head_par,
             "parity_all_ok": bool(all_ok),
@@ -764,8 +776,13 @@ def gpu_arm(args, sync, local) -> None:
                 # capture of this workload), details in traffic_detail
                 "traffic": (lambda tr: round(tr["dram_bytes_per_launch"]) if tr else None)(committed_traffic(pl)),
                 "traffic_detail": committed_traffic(pl),
-                "work_per_product": round(W, 1),
-                "work_model": "W_alg = 144 t^log2(3) + 4t (SURVEY §8(d)), t=ceil(n/64)",
+                "work_per_product": round(W_node, 1),
+                "work_model": ("W_alg = 144 t^log2(3) + 4t (SURVEY §8(d)), t=ceil(n/64)" if not TL else
+                               f"node kernel: 5^{TL} node problems per product x W_alg(t_node) = 144 t_node^log2(3), "
+                               f"t_node = {t_node:g} words (the plan's {TL} Toom-3 levels run in the memory passes); "
+                               "whole_step_frac charges the product's own W_alg = 144 t^log2(3) + 4t, "
+                               "t=ceil(n/64) (work_per_product_whole)"),
+                "work_per_product_whole": round(W, 1),
                 "peak_source": "live LOP3 microbenchmark (c^(a&b), 8 chains/thread, 8 CTAs/SM) this run",
                 "peak_nominal_L64": round(nominal, 3),
                 "frac_of_nominal_L64": round(achieved / nominal, 4),
@@ -798,7 +815,9 @@ def gpu_arm(args, sync, local) -> None:
             },
             "ncu_node_kernel": committed_ncu(pl),
             "paper_avx512_1core_products_s": round(PAPER_1CORE[N_RING], 1) if n == N_RING else None,
-            "gpu_launches": int((K + max(3, K // 2) * CHUNKS) * pl["launches"]),
+            # timed headline steps + e2e batches (each row chunk is its own call and plan)
+            "gpu_launches": int(K * pl["launches"] + max(3, K // 2) * CHUNKS *
+                                plan("cyclic", -(-bpg // CHUNKS), n, args.leaf)["launches"]),
             "clocks": cl,
         }
         if scaling:

@@ -71,7 +71,10 @@ def _row_chunks(lib, kind: int, batch: int, t_or_n: int, leaf: int) -> tuple[lis
         per = max(1, per * 7 // 8)
     rows = 32 * per
     chunks = [(lo, min(lo + rows, batch)) for lo in range(0, batch, rows)]
-    return chunks, int(lib.f2x_workspace_bytes(kind, rows, t_or_n, leaf))
+    # the plan depends on the chunk's group count: a shorter last chunk may take
+    # another plan, so size the scratch for every distinct chunk length
+    sizes = {hi - lo for lo, hi in chunks}
+    return chunks, max(int(lib.f2x_workspace_bytes(kind, r, t_or_n, leaf)) for r in sizes)
 
 
 def _check_operands(A: torch.Tensor, B: torch.Tensor) -> None:
@@ -384,7 +387,9 @@ class HostPipeline:
         # be shared with (or freed by) other callers of the same stream
         lib = _lib.load()
         kind_id = _lib.KIND_CYCLIC if kind == "cyclic" else _lib.KIND_FULL
-        self.ws_bytes = _row_chunks(lib, kind_id, rows, self.size, leaf)[1]
+        # (the plan depends on the chunk's group count: size for every chunk length)
+        self.ws_bytes = max(_row_chunks(lib, kind_id, hi - lo, self.size, leaf)[1]
+                            for lo, hi in set((0, b - a) for a, b in self.bounds))
         for _ in range(max(1, lanes)):
             ss = [torch.cuda.Stream(self.device) for _ in range(nstreams)]
             bufs = [(torch.empty((rows, self.t), dtype=torch.int64, device=self.device),
