@@ -115,7 +115,7 @@ def committed_traffic(pl) -> dict | None:
             d = json.load(open(f))
         except Exception:
             continue
-        if (d.get("workload") == "n=17669 x4096" and
+        if (d.get("workload") == "n=17669 x4096" and pl.get("n") == 17669 and pl.get("batch") == 4096 and
                 d.get("kernel") == f"k2_node_mul<{pl['leaf_words']},{pl['cta_levels']}>" and
                 d.get("grid", pl["node_ctas"]) == pl["node_ctas"]):
             # algorithmic: both (pre-evaluated) bitsliced node-problem operands read
