@@ -47,15 +47,19 @@ static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
 static constexpr int kToomW = 16;       // x = X^w (coefficients)
-static constexpr double kToomWordCost = 15.0;  // planner: cost units per word moved (fit on B200)
-static constexpr int kToomMinWords = 512;      // Toom at any batch from 512 words: d=32768 (t=512) 27.26 -> 25.79 ms with two levels (round 2)
-// Below 512 words Toom pays only when its passes fill the GPU (measured, us per
-// call, TL 0/1/2: n=17669 x 2048 167/201/177 but x 4096 324/365/311 and x 16384
-// 1260/1422/1171; n=20000 x 4096 456/432/358; n=12323 x 4096 213/201/218; n=10000
-// 161/162/164; n=8000 108/128/118): considered from 160 words and 128 groups.
-static constexpr int kToomMinWordsBatched = 160;
-static constexpr int64_t kToomMinGroupsBatched = 128;
-static constexpr double kPassWordCost = 16.0;  // planner: global Karatsuba passes / slicing output, per word (n=17669 k3_interp<4>: 18.9 us for 128 x 223.5 K words)
+// Planner cost constants, in units of one leaf LOP3 per 32-product group
+// (3.8e-5 ns on B200), from a least-squares fit of 130 measured calls (ring
+// sizes 8000..57637 bits x 256..16384 rows x 0..3 Toom levels, DESIGN §7b
+// "planner regret"): mean regret of the picks 0.1 %, worst 2.5 %.
+static constexpr double kPassWordCost = 21.5;        // per word of the global Karatsuba passes / slicing output
+static constexpr double kToomWordCost = 10.5;        // per word the Toom passes move, plans of >= 2 levels
+static constexpr double kToomWordCostSingle = 21.0;  // same for one-level plans (one product per group and level: latency-bound)
+static constexpr double kToomLevelLatency = 2.63e8;  // per Toom level and CALL (~10 us: two more launches that cannot fill the GPU at small batches)
+// Toom is considered from 160 words (n=10000: 0 / 1 / 2 levels tie; d=8192
+// 11996 / 14350 / 12530 us); below 512 words it used to be off (round 1/2:
+// the passes were slower) -- n=17669 x 4096 now takes two levels (323.7 ->
+// 310.9 us), n=20000 x 4096 456 -> 358, while n=17669 x 2048 stays at 0.
+static constexpr int kToomMinWords = 160;
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -1590,13 +1594,13 @@ static double karatsuba_pass_words(int kind, int t, int TL, int LF, int K, int64
     return w;
 }
 
-static bool toom_considered(int t, int64_t G) {
-    return t >= kToomMinWords || (t >= kToomMinWordsBatched && G >= kToomMinGroupsBatched);
-}
+static bool toom_considered(int t) { return t >= kToomMinWords; }
 
 // Modelled cost per 32-product group of the best (LF, K) under TL Toom-3
 // levels (cost units: ~one leaf LOP3 per group): node kernel (best_leaf), the
-// global Karatsuba passes and slicing output, and the Toom passes.
+// global Karatsuba passes and slicing output, the Toom passes, and the
+// call's share of the per-level launch latency (so the depth depends on the
+// batch: small batches stay Karatsuba-only).
 static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, int &LF, int &K, int64_t *M,
                            double &c) {
     const int64_t Nmin = int64_t(64) * t;
@@ -1606,13 +1610,14 @@ static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, in
     c += kPassWordCost * karatsuba_pass_words(kind, t, TL, LF, K, G, M);
     c *= double(ipow5(TL));
     if (TL > 0) c += kPassWordCost * 2.0 * 3.0 * double(M[1]);  // plain bitsliced slice (k1_slice)
-    // Toom passes are HBM-bound: ~kToomWordCost per word moved per group
+    // Toom passes: HBM-bound per word moved, plus a per-call latency per level
     for (int l = 1; l <= TL; ++l) {
         const double Sl = l < TL ? 3.0 * double(M[l + 1]) : double(int64_t(LF) << K);
         const double ev = 2.0 * double(ipow5(l - 1)) * 3.0 * double(M[l]) + 2.0 * double(ipow5(l)) * Sl;
         const double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
-        c += kToomWordCost * (ev + ip);
+        c += (TL == 1 ? kToomWordCostSingle : kToomWordCost) * (ev + ip);
     }
+    c += kToomLevelLatency * double(TL) / double(G);
     return true;
 }
 
@@ -1640,7 +1645,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     const int64_t Gp = ceil_div(batch, 32);
     for (int TL = 0; TL <= kMaxToom; ++TL) {
         if (forced >= 0 && TL != forced) continue;
-        if (TL > 0 && (leaf_hint || (forced < 0 && !toom_considered(t, Gp)))) continue;
+        if (TL > 0 && (leaf_hint || (forced < 0 && !toom_considered(t)))) continue;
         int64_t M[kMaxToom + 1] = {0};
         int LF, K;
         double c;

@@ -200,28 +200,50 @@ def test_bench_two_gpus_spawned(cuda):
     assert "NCCL INFO" not in r.stdout + r.stderr  # no NCCL communicator was created
 
 
+def _random_cases():
+    """(kind, size, batch) draws of test_random_sizes_vs_oracle: small batches
+    (Karatsuba-only plans: the Toom passes cannot fill the GPU) and batches
+    of 1000-4200 rows (the planner's Toom depths)."""
+    rng = np.random.default_rng(0x5EED)
+    cases = []
+    for i in range(28):
+        n = int(rng.integers(1, 70000))
+        batch = int(rng.integers(1, 48)) if i % 2 == 0 else int(rng.integers(1000, 4200))
+        cases.append(("cyclic", n, batch))
+    for i in range(16):
+        t = int(rng.integers(1, 1536))
+        batch = int(rng.integers(1, 40)) if i % 2 == 0 else int(rng.integers(1000, 2100))
+        cases.append(("full", t, batch))
+    return cases
+
+
+def test_random_cases_reach_every_toom_depth():
+    """The seeded draws cover Karatsuba-only plans and 1, 2 and 3 Toom-3 levels
+    (the plan is host-only: checked without a GPU too)."""
+    from paper_2201_10473_b200 import plan
+
+    seen = {plan(kind, batch, size)["toom_levels"] for kind, size, batch in _random_cases()}
+    assert seen == {0, 1, 2, 3}, seen
+
+
 def test_random_sizes_vs_oracle(cuda):
     """Seeded random ring sizes (1 .. 70000 bits, every Toom / leaf / chunk
     regime the planner reaches) and full-product sizes (1 .. 1536 words)
-    with random batch sizes, against the C oracle."""
+    with random batch sizes, against the C oracle (all rows of the small
+    batches; the first and last 8 rows and 16 random rows of the large)."""
     from oracle import c_mul_cyclic, c_mul_full
     from oracle.f2x_oracle import make_cyclic_inputs, make_full_inputs
-    from paper_2201_10473_b200 import mul_cyclic, mul_full, plan
+    from paper_2201_10473_b200 import mul_cyclic, mul_full
 
-    rng = np.random.default_rng(0x5EED)
-    seen_toom = set()
-    for _ in range(24):
-        n = int(rng.integers(1, 70000))
-        batch = int(rng.integers(1, 48))
-        A, B = make_cyclic_inputs(n, batch)
-        got = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), n))
-        assert np.array_equal(got, c_mul_cyclic(A, B, n)), (n, batch)
-        seen_toom.add(plan("cyclic", batch, n)["toom_levels"])
-    for _ in range(16):
-        t = int(rng.integers(1, 1536))
-        batch = int(rng.integers(1, 40))
-        A, B = make_full_inputs(t, batch, words=True)
-        got = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
-        assert np.array_equal(got, c_mul_full(A, B)), (t, batch)
-        seen_toom.add(plan("full", batch, t)["toom_levels"])
-    assert {0, 1, 2} <= seen_toom or {0, 2} <= seen_toom, seen_toom
+    rng = np.random.default_rng(0xC0FFEE)
+    for kind, size, batch in _random_cases():
+        if kind == "cyclic":
+            A, B = make_cyclic_inputs(size, batch)
+            got = _np(mul_cyclic(_dev(A, cuda), _dev(B, cuda), size))
+        else:
+            A, B = make_full_inputs(size, batch, words=True)
+            got = _np(mul_full(_dev(A, cuda), _dev(B, cuda)))
+        rows = np.arange(batch) if batch <= 48 else np.unique(np.r_[0:8, batch - 8:batch,
+                                                                     rng.integers(0, batch, 16)])
+        want = c_mul_cyclic(A[rows], B[rows], size) if kind == "cyclic" else c_mul_full(A[rows], B[rows])
+        assert np.array_equal(got[rows], want), (kind, size, batch)

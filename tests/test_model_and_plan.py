@@ -127,13 +127,17 @@ def test_plan_struct_size_matches_header(lib):
 
 
 # (kind, batch, t_or_n) -> Toom-3 levels measured fastest on B200 (DESIGN §7b
-# "planner regret"; tools/runs/toomgrid2.sh): the picks below 512 words need
-# 128 groups to fill the GPU with the Toom passes
+# "planner regret"; tools/runs/toomgrid2.sh, toomgate.sh, toomsmall.sh): the
+# depth depends on the batch -- the Toom passes add ~10 us of latency per level
+# and call, so small batches stay Karatsuba-only
 PLANNER_PINS = [
-    (1, 256, 12323, 0), (1, 4096, 12323, 1), (1, 2048, 17669, 0), (1, 4096, 17669, 2),
-    (1, 16384, 17669, 2), (1, 4096, 9000, 0), (1, 4096, 14000, 2), (1, 4096, 20000, 2),
-    (1, 4096, 24000, 1), (1, 4096, 28000, 3), (1, 4096, 32000, 2), (1, 4096, 35851, 2),
-    (1, 16384, 57637, 3), (0, 1 << 20, 64, 0), (0, 1 << 19, 128, 0), (0, 1 << 18, 256, 0),
+    (1, 256, 12323, 0), (1, 2048, 12323, 0), (1, 3072, 12323, 1), (1, 4096, 12323, 1),
+    (1, 256, 17669, 0), (1, 2048, 17669, 0), (1, 3072, 17669, 2), (1, 4096, 17669, 2),
+    (1, 16384, 17669, 2), (1, 4096, 9000, 0), (1, 4096, 14000, 2), (1, 1024, 20000, 2),
+    (1, 4096, 20000, 2), (1, 1024, 24000, 1), (1, 4096, 22000, 3), (1, 2048, 28000, 3),
+    (1, 4096, 28000, 3), (1, 4096, 30000, 2), (1, 32, 35851, 0), (1, 256, 35851, 0),
+    (1, 1024, 35851, 2), (1, 4096, 35851, 2), (1, 32, 57637, 0), (1, 256, 57637, 3),
+    (1, 16384, 57637, 3), (0, 1 << 20, 64, 0), (0, 1 << 19, 128, 0), (0, 1 << 18, 256, 2),
     (0, 1 << 17, 512, 2), (0, 1 << 16, 1024, 2),
 ]
 
@@ -421,10 +425,12 @@ def test_plan_resident_root_launches(lib):
     products): one launch fewer.  n=35851's last pass has two levels."""
     from paper_2201_10473_b200 import _lib
 
-    for batch, fused in ((16384, True), (160, True), (40, False)):
+    for batch in (16384, 1024, 256):
         pl = _lib.make_plan(_lib.KIND_CYCLIC, batch, 57637)
         assert pl.toom_levels == 3 and pl.num_passes == 1 and pl.pass_levels[0] == 1
-        assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels - (1 if fused else 0), batch
+        assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels - 1, batch
+    # (batches whose innermost level has < 96 products take no Toom level at all)
+    assert _lib.make_plan(_lib.KIND_CYCLIC, 40, 57637).toom_levels == 0
     pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 35851)
     assert pl.launches == 3 + pl.num_passes + 2 * pl.toom_levels
 
@@ -432,11 +438,11 @@ def test_plan_resident_root_launches(lib):
 def test_plan_k34_fusion_launches(lib):
     """The last global pass is fused with the unslicing kernel (k34) for
     Karatsuba-only plans with >= 1024 groups, a last pass of <= 3 levels and
-    a root stage of <= 72 KB: d-sweep d=4096 / 8192 yes, d=16384 (4 levels)
-    and n=17669 x 2048 (64 groups) no."""
+    a root stage of <= 72 KB: d-sweep d=4096 / 8192 yes, d=4096 x 4096 (128
+    groups) and n=17669 x 2048 (64 groups, 4 levels) no."""
     from paper_2201_10473_b200 import _lib
 
-    for t, batch, fused in ((64, 1 << 20, True), (128, 1 << 19, True), (256, 1 << 18, False), (64, 4096, False)):
+    for t, batch, fused in ((64, 1 << 20, True), (128, 1 << 19, True), (64, 4096, False)):
         pl = _lib.make_plan(_lib.KIND_FULL, batch, t)
         assert pl.toom_levels == 0
         assert pl.launches == 3 + pl.num_passes - (1 if fused else 0), (t, batch)
