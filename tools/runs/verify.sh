@@ -5,4 +5,3 @@ timeout 2000 python -m pytest tests -m gpu -q -rfEs > gpurun_out/gputest.log 2>&
 timeout 900 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 300 python tools/kernel_times.py 17669 35851 57637:16384 12323:256 > gpurun_out/ktimes.log 2>&1
 tail -n 3 gpurun_out/smoke.log gpurun_out/gputest.log gpurun_out/bench.err
-F2X_KROOT=0 timeout 300 python tools/kernel_times.py 17669 14000 20000 > gpurun_out/kroot0.log 2>&1
