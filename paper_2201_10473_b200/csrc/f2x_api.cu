@@ -46,7 +46,7 @@ static constexpr int kMaxGL = 8;
 static constexpr int kMaxPassLevels = 4;
 static constexpr int kThreads = 128;
 static constexpr int kMaxToom = 3;      // Toom-3 levels above the node problem
-static constexpr int kToomW = 16;      // x = X^w (coefficients)
+static constexpr int kToomW = 16;       // x = X^w (coefficients)
 // Planner cost constants, in units of one leaf LOP3 per 32-product group
 // (3.8e-5 ns on B200), from a least-squares fit of 130 measured calls (ring
 // sizes 8000..57637 bits x 256..16384 rows x 0..3 Toom levels, DESIGN §7b
