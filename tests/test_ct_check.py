@@ -95,7 +95,11 @@ d = lambda x: torch.from_numpy(x.view(np.int64)).cuda()
 assert np.array_equal(mul_cyclic(d(A), d(B), 17669).cpu().numpy().view(np.uint64), c_mul_cyclic(A, B, 17669))
 print(json.dumps(ct_check(n=17669, weight=75, trials=10_000)))
 """
-    env = dict(os.environ, F2X_LIB_VARIANT="leaky")
+    # Karatsuba-only plan: the leaves see the sparse operand itself (a ~4 % leak).
+    # Under the default two Toom-3 levels the evaluated node operands are
+    # denser, the same fixture leaks ~0.8 % -- still |t| > 10, but too close to
+    # the 1 % size bound below to pin.
+    env = dict(os.environ, F2X_LIB_VARIANT="leaky", F2X_TOOM="0")
     r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
