@@ -81,6 +81,8 @@ typedef struct f2x_plan {
                                 (node kernel runs on 5^toom_levels x groups) */
     int32_t toom_w;          /* Toom-3 point x = X^toom_w                      */
     int32_t toom_M[4];       /* part size (coefficients) of Toom level 1..     */
+    int32_t toom_w_last;     /* w of the innermost Toom level (toom_w or 8): the
+                                node problem holds toom_M[last] + 2 toom_w_last */
 } f2x_plan;
 
 /* Fill *plan for a call shape.  leaf_hint = 0 picks the default leaf;

@@ -70,6 +70,7 @@ class F2xPlan(ctypes.Structure):
         ("toom_levels", ctypes.c_int32),
         ("toom_w", ctypes.c_int32),
         ("toom_M", ctypes.c_int32 * 4),
+        ("toom_w_last", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

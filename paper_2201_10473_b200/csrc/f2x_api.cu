@@ -60,6 +60,12 @@ static constexpr double kToomLevelLatency = 2.63e8;  // per Toom level and CALL 
 // the passes were slower) -- n=17669 x 4096 now takes two levels (323.7 ->
 // 310.9 us), n=20000 x 4096 456 -> 358, while n=17669 x 2048 stays at 0.
 static constexpr int kToomMinWords = 160;
+// The innermost Toom level may evaluate at x = X^8 instead of X^16: the node
+// problem then holds M_TL + 16 instead of + 32 coefficients, which at some
+// sizes is one leaf word less (n=57637: LF 35 -> 34); its interpolation scans
+// twice the segments per block (measured +8..13 %), charged below.
+static constexpr int kToomWSmall = 8;
+static constexpr double kToomSmallWInterpPenalty = 1.25;  // (1.2 .. 1.3 give the measured-best picks: d=32768 stays at w = 16)
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -354,6 +360,7 @@ struct ToomEvalGeo {
     int Tc;         // chunks per tile (Tc LF multiple of 4)
     int64_t G;      // groups
     int64_t Ns;     // storage words per node-problem operand
+    int wl;         // w of the innermost level's point x = X^wl (<= kToomW; windows keep the 2 kToomW halo)
 };
 
 constexpr int kEvalFusedThreads = 256;
@@ -469,6 +476,7 @@ __global__ void __launch_bounds__(kEvalFusedThreads, 3)
 toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint32_t *__restrict__ Yb,
                 const ToomEvalGeo geo, int64_t x0_words) {
     constexpr int w = kToomW;
+    const int wl = geo.wl;  // the final level's point (its window still starts 2w before the tile)
     constexpr int NP0 = efpow3(TL), Z0 = efslot(TL, 0);
     extern __shared__ __align__(16) uint32_t efs[];
     __shared__ __align__(8) uint64_t mbar;
@@ -570,11 +578,11 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
                 const int j = fj0[u] + r, k = k0 + j;
                 const bool data = (fdm[u] >> r) & 1u;
                 const bool ka = data && (interior || unsigned(k) < unsigned(Mt));
-                const bool k1 = data && (interior || unsigned(k - w) < unsigned(Mt));
-                const bool k2 = data && (interior || unsigned(k - 2 * w) < unsigned(Mt));
+                const bool k1 = data && (interior || unsigned(k - wl) < unsigned(Mt));
+                const bool k2 = data && (interior || unsigned(k - 2 * wl) < unsigned(Mt));
                 const uint32_t a0 = ka ? P0[j + 2 * w] : 0u, a1 = ka ? P1[j + 2 * w] : 0u,
                                a2 = ka ? P2[j + 2 * w] : 0u;
-                const uint32_t s1 = k1 ? P1[j + w] : 0u, s2 = k2 ? P2[j] : 0u;
+                const uint32_t s1 = k1 ? P1[j + 2 * w - wl] : 0u, s2 = k2 ? P2[j + 2 * w - 2 * wl] : 0u;
                 const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
                 v[0][r] = a0;
                 v[1][r] = p1;
@@ -597,11 +605,11 @@ toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint
             for (int r = 0; r < 4; ++r) {
                 const int j = c * LF + r0 + r, k = k0 + j;
                 const bool data = r0 + r < LF;
-                const bool ka = data && unsigned(k) < unsigned(Mt), k1 = data && unsigned(k - w) < unsigned(Mt),
-                           k2 = data && unsigned(k - 2 * w) < unsigned(Mt);
+                const bool ka = data && unsigned(k) < unsigned(Mt), k1 = data && unsigned(k - wl) < unsigned(Mt),
+                           k2 = data && unsigned(k - 2 * wl) < unsigned(Mt);
                 const uint32_t a0 = ka ? L0[j + 2 * w] : 0u, a1 = ka ? L0[Z0 + j + 2 * w] : 0u,
                                a2 = ka ? L0[2 * Z0 + j + 2 * w] : 0u;
-                const uint32_t s1 = k1 ? L0[Z0 + j + w] : 0u, s2 = k2 ? L0[2 * Z0 + j] : 0u;
+                const uint32_t s1 = k1 ? L0[Z0 + j + 2 * w - wl] : 0u, s2 = k2 ? L0[2 * Z0 + j + 2 * w - 2 * wl] : 0u;
                 const uint32_t p1 = a0 ^ a1 ^ a2, xs = s1 ^ s2;
                 v[0][r] = a0;
                 v[1][r] = p1;
@@ -831,13 +839,13 @@ __host__ __device__ constexpr int kres_words(int nb, int blk) {
 // straight into R (first contribution to a coefficient written, the second
 // added by an L2 XOR reduction): no c_j round trip through HBM, one launch.
 // NT = 512 (with BLK = 4096) for levels with at most one product per SM.
-template <int BLK, bool RES, int NT = kToomScanT>
+template <int BLK, bool RES, int NT = kToomScanT, int W = kToomW>
 __global__ void __launch_bounds__(NT, RES ? 2 : (NT > 256 ? 1 : 3))
 toom_interp_seq(const uint32_t *__restrict__ Cin, uint32_t *__restrict__ R, int M, int LFi, int LFSi, int64_t inS,
                 int Lin, int64_t outS, const KRootIn kr) {
     extern __shared__ uint32_t tsm[];
-    constexpr int W = kToomW, ROWS = BLK / W, NSEG = NT / W, SEGR = ROWS / NSEG;
-    constexpr int H = BLK + 3 * W;
+    constexpr int ROWS = BLK / W, NSEG = NT / W, SEGR = ROWS / NSEG;
+    constexpr int H = BLK + 3 * W;  // (W <= kToomW: the strides below are sized for kToomW)
     const int HP = RES ? kr.hp : toom_stg_stride(BLK);  // padded stride per input (see tstg)
     uint32_t *Stg = tsm;  // [5][HP]
     __shared__ uint32_t stot[3][NSEG][W];
@@ -1385,6 +1393,7 @@ struct Layout {
     int64_t off_abs, off_bbs, off_p0, off_p1, total;
     int el;                          // pre-evaluated top global levels (K1b)
     int tl = 0;                      // Toom-3 levels
+    int wl = 16;                     // w of the innermost Toom level (x = X^wl)
     int64_t G2 = 0;                  // node-problem groups (G 5^tl)
     int64_t M[kMaxToom + 1] = {};    // Toom part sizes, level 1..tl
     int64_t off_x0 = 0;              // Toom plans: plain bitsliced slice (both operands)
@@ -1445,12 +1454,12 @@ static bool best_leaf(int64_t Smin, int leaf_hint, int &bestLF, int &bestK, doub
 // into thirds and evaluates at 0, 1, x, x+1, inf (x = X^w): 5 operands of
 // S_l >= M_l + 2w coefficients; S_l = 3 M_{l+1} below another Toom level,
 // the node size LF 2^K at the last.  Sizes for Nmin coefficients:
-static void toom_sizes(int64_t Nmin, int TL, int64_t *M, int64_t &Smin_last) {
+static void toom_sizes(int64_t Nmin, int TL, int wl, int64_t *M, int64_t &Smin_last) {
     // multiples of 4 coefficients: every Toom piece is a whole 16-byte quad
     // (toom_eval_fused); costs <= 3 coefficients of padding per level
     M[1] = (ceil_div(Nmin, 3) + 3) & ~int64_t(3);
     for (int l = 1; l < TL; ++l) M[l + 1] = (ceil_div(M[l] + 2 * kToomW, 3) + 3) & ~int64_t(3);
-    Smin_last = M[TL] + 2 * kToomW;
+    Smin_last = M[TL] + 2 * wl;  // the innermost level evaluates at x = X^wl (kToomW or kToomWSmall)
 }
 
 // Toom interpolation: levels with >= this many products use the one-CTA-per-
@@ -1596,17 +1605,23 @@ static double karatsuba_pass_words(int kind, int t, int TL, int LF, int K, int64
 
 static bool toom_considered(int t) { return t >= kToomMinWords; }
 
-// Modelled cost per 32-product group of the best (LF, K) under TL Toom-3
-// levels (cost units: ~one leaf LOP3 per group): node kernel (best_leaf), the
-// global Karatsuba passes and slicing output, the Toom passes, and the
-// call's share of the per-level launch latency (so the depth depends on the
-// batch: small batches stay Karatsuba-only).
-static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, int &LF, int &K, int64_t *M,
-                           double &c) {
+static int toom_wlast_override() {  // F2X_TOOM_WLAST=8|16 forces the innermost level's w (experiments / tests)
+    static const int v = [] {
+        const char *e = getenv("F2X_TOOM_WLAST");
+        const int x = e ? atoi(e) : 0;
+        return (x == kToomW || x == kToomWSmall) ? x : 0;
+    }();
+    return v;
+}
+
+static bool plan_candidate_w(int kind, int t, int TL, int wl, int leaf_hint, int64_t G, int &LF, int &K,
+                             int64_t *M, double &c) {
     const int64_t Nmin = int64_t(64) * t;
     int64_t Smin = Nmin;
-    if (TL > 0) toom_sizes(Nmin, TL, M, Smin);
+    if (TL > 0) toom_sizes(Nmin, TL, wl, M, Smin);
     if (!best_leaf(Smin, TL > 0 && toom_leaf_override() ? toom_leaf_override() : leaf_hint, LF, K, c)) return false;
+    // the small point needs the one-CTA-per-product interpolation at the innermost level
+    if (TL > 0 && wl != kToomW && !toom_use_seq(G * ipow5(TL - 1), M[TL])) return false;
     c += kPassWordCost * karatsuba_pass_words(kind, t, TL, LF, K, G, M);
     c *= double(ipow5(TL));
     if (TL > 0) c += kPassWordCost * 2.0 * 3.0 * double(M[1]);  // plain bitsliced slice (k1_slice)
@@ -1614,11 +1629,41 @@ static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, in
     for (int l = 1; l <= TL; ++l) {
         const double Sl = l < TL ? 3.0 * double(M[l + 1]) : double(int64_t(LF) << K);
         const double ev = 2.0 * double(ipow5(l - 1)) * 3.0 * double(M[l]) + 2.0 * double(ipow5(l)) * Sl;
-        const double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
+        double ip = 3.0 * double(ipow5(l)) * 2.0 * Sl + 1.5 * double(ipow5(l - 1)) * 6.0 * double(M[l]);
+        if (l == TL && wl != kToomW) ip *= kToomSmallWInterpPenalty;
         c += (TL == 1 ? kToomWordCostSingle : kToomWordCost) * (ev + ip);
     }
     c += kToomLevelLatency * double(TL) / double(G);
     return true;
+}
+
+// Modelled cost per 32-product group of the best (LF, K, innermost w) under TL
+// Toom-3 levels (cost units: ~one leaf LOP3 per group): node kernel
+// (best_leaf), the global Karatsuba passes and slicing output, the Toom
+// passes, and the call's share of the per-level launch latency (so the depth
+// depends on the batch: small batches stay Karatsuba-only).
+static bool plan_candidate(int kind, int t, int TL, int leaf_hint, int64_t G, int &LF, int &K, int64_t *M,
+                           double &c, int &wl) {
+    bool any = false;
+    const int forced = toom_wlast_override();
+    for (int w : {kToomWSmall, kToomW}) {
+        if (TL == 0 && w != kToomW) continue;
+        if (TL > 0 && forced && w != forced && !(w == kToomW && forced == kToomWSmall)) continue;
+        if (TL > 0 && forced == kToomWSmall && w == kToomW && any) continue;  // (kToomW only as the fallback)
+        int lf, k;
+        int64_t m[kMaxToom + 1] = {0};
+        double cc;
+        if (!plan_candidate_w(kind, t, TL, w, leaf_hint, G, lf, k, m, cc)) continue;
+        if (!any || cc < c) {
+            any = true;
+            c = cc;
+            LF = lf;
+            K = k;
+            wl = w;
+            std::memcpy(M, m, sizeof(m));
+        }
+    }
+    return any;
 }
 
 static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_plan *pl,
@@ -1638,7 +1683,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     }
     const int64_t Nmin = int64_t(64) * t;
     // candidates: 0..kMaxToom Toom-3 levels on top of the Karatsuba node problem
-    int bestTL = -1, bestLF = 0, bestK = 0;
+    int bestTL = -1, bestLF = 0, bestK = 0, bestWl = kToomW;
     double best = 0;
     int64_t bestM[kMaxToom + 1] = {0};
     const int forced = leaf_hint ? 0 : toom_override();
@@ -1647,14 +1692,15 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         if (forced >= 0 && TL != forced) continue;
         if (TL > 0 && (leaf_hint || (forced < 0 && !toom_considered(t)))) continue;
         int64_t M[kMaxToom + 1] = {0};
-        int LF, K;
+        int LF, K, wl = kToomW;
         double c;
-        if (!plan_candidate(kind, t, TL, leaf_hint, Gp, LF, K, M, c)) continue;
+        if (!plan_candidate(kind, t, TL, leaf_hint, Gp, LF, K, M, c, wl)) continue;
         if (bestTL < 0 || c < best) {
             best = c;
             bestTL = TL;
             bestLF = LF;
             bestK = K;
+            bestWl = wl;
             std::memcpy(bestM, M, sizeof(M));
         }
     }
@@ -1690,6 +1736,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     pl->node_smem_bytes = int64_t(e->smem);
     pl->toom_levels = TL;
     pl->toom_w = TL ? kToomW : 0;
+    pl->toom_w_last = TL ? bestWl : 0;
     for (int l = 1; l <= TL; ++l) pl->toom_M[l - 1] = int32_t(bestM[l]);
     // analytic operation counts per product (bitsliced: 1 LOP3 = 32 products)
     pl->leaf_ops_per_product = double(ipow5(TL)) * double(ipow3(K)) * LF * LF / 32.0;
@@ -1706,6 +1753,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     }
     Layout L;
     L.tl = TL;
+    L.wl = TL ? bestWl : kToomW;
     L.G2 = G2;
     for (int l = 0; l <= kMaxToom; ++l) L.M[l] = bestM[l];
     L.Ns = int64_t(LFS) << K;
@@ -1883,6 +1931,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         geo.Tc = 8 * pl.leaf_words <= kEvalFusedMaxT ? 8 : 4;
         geo.G = G;
         geo.Ns = L.Ns;
+        geo.wl = L.wl;
         const int etiles = int(ceil_div(geo.chunks, geo.Tc));
         const size_t sm = size_t(eval_fused_smem_words(L.tl)) * 4;
         static std::atomic<uint32_t> ef_dev_mask{0};
@@ -2072,50 +2121,48 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         if (dev < 31 && !(attr_dev_mask.load() & (1u << dev))) {
             cudaError_t ae = cudaFuncSetAttribute(toom_interp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   int(sms));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(5 * toom_stg_stride(2048) * 4));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2304, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(5 * toom_stg_stride(2304) * 4));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<4096, false, 512>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(5 * toom_stg_stride(4096) * 4));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2048, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kResSmemMax);
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_interp_seq<2304, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kResSmemMax);
+#define F2X_SEQ_ATTR(BLK, RES, NT, BYTES)                                                                      \
+    if (ae == cudaSuccess)                                                                                    \
+        ae = cudaFuncSetAttribute(toom_interp_seq<BLK, RES, NT, kToomW>,                                      \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(BYTES));                   \
+    if (ae == cudaSuccess)                                                                                    \
+        ae = cudaFuncSetAttribute(toom_interp_seq<BLK, RES, NT, kToomWSmall>,                                 \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(BYTES));
+            F2X_SEQ_ATTR(2048, false, kToomScanT, 5 * toom_stg_stride(2048) * 4)
+            F2X_SEQ_ATTR(2304, false, kToomScanT, 5 * toom_stg_stride(2304) * 4)
+            F2X_SEQ_ATTR(4096, false, 512, 5 * toom_stg_stride(4096) * 4)
+            F2X_SEQ_ATTR(2048, true, kToomScanT, kResSmemMax)
+            F2X_SEQ_ATTR(2304, true, kToomScanT, kResSmemMax)
+#undef F2X_SEQ_ATTR
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             attr_dev_mask.fetch_or(1u << dev);
         }
         if (seq) {
             const bool res = kroot && l == L.tl;  // roots built in shared memory from the path products
             const size_t smr = res ? size_t(5) * kr.hp * 4 : 0;
+            // the innermost level's point may be x = X^8 (planner: only with this one-CTA-per-product form)
+            const bool small_w = l == L.tl && L.wl == kToomWSmall;
+#define F2X_SEQ_LAUNCH(BLK, RES, NT, BYTES)                                                                   \
+    do {                                                                                                      \
+        if (small_w)                                                                                          \
+            F2X_LAUNCH((toom_interp_seq<BLK, RES, NT, kToomWSmall>), unsigned(items), NT, BYTES, stream, root, out, \
+                       M, rootLF, rootLFS, rootS, Lin, outS, kr);                                             \
+        else                                                                                                  \
+            F2X_LAUNCH((toom_interp_seq<BLK, RES, NT, kToomW>), unsigned(items), NT, BYTES, stream, root, out, M,   \
+                       rootLF, rootLFS, rootS, Lin, outS, kr);                                                \
+    } while (0)
             if (!res && items <= kWideSeqMaxItems && 2 * M > 4096) {
                 // at most one product per SM: 512 threads walk 4096-coefficient
                 // blocks (half the sequential block steps of the 256-thread form)
-                F2X_LAUNCH((toom_interp_seq<4096, false, 512>), unsigned(items), 512, 5 * toom_stg_stride(4096) * 4,
-                           stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS, kr);
+                F2X_SEQ_LAUNCH(4096, false, 512, 5 * toom_stg_stride(4096) * 4);
             } else if (toom_seq_blk(M) == 2304) {
-                if (res)
-                    F2X_LAUNCH((toom_interp_seq<2304, true>), unsigned(items), kToomScanT, smr, stream, root, out, M,
-                               rootLF, rootLFS, rootS, Lin, outS, kr);
-                else
-                    F2X_LAUNCH((toom_interp_seq<2304, false>), unsigned(items), kToomScanT,
-                               5 * toom_stg_stride(2304) * 4, stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS,
-                               kr);
+                if (res) F2X_SEQ_LAUNCH(2304, true, kToomScanT, smr);
+                else F2X_SEQ_LAUNCH(2304, false, kToomScanT, 5 * toom_stg_stride(2304) * 4);
             } else {
-                if (res)
-                    F2X_LAUNCH((toom_interp_seq<2048, true>), unsigned(items), kToomScanT, smr, stream, root, out, M,
-                               rootLF, rootLFS, rootS, Lin, outS, kr);
-                else
-                    F2X_LAUNCH((toom_interp_seq<2048, false>), unsigned(items), kToomScanT,
-                               5 * toom_stg_stride(2048) * 4, stream, root, out, M, rootLF, rootLFS, rootS, Lin, outS,
-                               kr);
+                if (res) F2X_SEQ_LAUNCH(2048, true, kToomScanT, smr);
+                else F2X_SEQ_LAUNCH(2048, false, kToomScanT, 5 * toom_stg_stride(2048) * 4);
             }
+#undef F2X_SEQ_LAUNCH
             if ((rc = debug_sync(stream, 5))) return rc;
         } else {
             F2X_LAUNCH(toom_interp_scan, unsigned(items * nb), kToomScanT, sms, stream, root, Q, Tot, M, kToomW, rootLF,
@@ -2199,7 +2246,8 @@ double f2x_plan_cost(int32_t kind, int64_t batch, int32_t t_or_n, int32_t toom_l
     int64_t M[f2x::kMaxToom + 1] = {0};
     int LF, K;
     double c;
-    if (!f2x::plan_candidate(kind, t, toom_levels, 0, f2x::ceil_div(batch, 32), LF, K, M, c)) return -1.0;
+    int wl;
+    if (!f2x::plan_candidate(kind, t, toom_levels, 0, f2x::ceil_div(batch, 32), LF, K, M, c, wl)) return -1.0;
     return c;
 }
 

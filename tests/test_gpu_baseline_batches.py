@@ -247,3 +247,38 @@ def test_random_sizes_vs_oracle(cuda):
                                                                      rng.integers(0, batch, 16)])
         want = c_mul_cyclic(A[rows], B[rows], size) if kind == "cyclic" else c_mul_full(A[rows], B[rows])
         assert np.array_equal(got[rows], want), (kind, size, batch)
+
+
+@pytest.mark.parametrize("tl,n,batch", [(1, 12323, 4096), (2, 17669, 4096), (2, 20000, 4096), (2, 35851, 4096),
+                                         (3, 28000, 3072), (3, 57637, 1024), (2, 1000, 4000)])
+def test_innermost_point_x8_vs_oracle(cuda, tl, n, batch):
+    """The innermost Toom level at x = X^8 (F2X_TOOM_WLAST=8, read once per
+    process: subprocess) for every interpolation form it can take -- resident
+    roots with 2048 / 2304 blocks, plain roots, the 512-thread form, 1..3
+    levels -- against the C oracle on the first / last 8 and 48 random rows."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+n, batch, tl = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+from oracle import c_mul_cyclic
+from oracle.f2x_oracle import make_cyclic_inputs
+from paper_2201_10473_b200 import mul_cyclic, plan
+p = plan("cyclic", batch, n)
+assert p["toom_levels"] == tl and p["toom_w_last"] == 8, p
+assert p["leaf_words"] << p["levels"] >= p["toom_M"][-1] + 16
+A, B = make_cyclic_inputs(n, batch)
+d = lambda x: torch.from_numpy(x.view(np.int64)).cuda()
+got = mul_cyclic(d(A), d(B), n).cpu().numpy().view(np.uint64)
+rows = np.unique(np.r_[0:8, batch - 8:batch, np.random.default_rng(n).integers(0, batch, 48)])
+assert np.array_equal(got[rows], c_mul_cyclic(A[rows], B[rows], n))
+print("ok")
+"""
+    env = dict(os.environ, F2X_TOOM_WLAST="8", F2X_TOOM=str(tl))
+    r = subprocess.run([sys.executable, "-c", script, root, str(n), str(batch), str(tl)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]

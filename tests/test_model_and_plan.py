@@ -120,7 +120,7 @@ def test_plan_struct_size_matches_header(lib):
     pl = _lib.make_plan(_lib.KIND_CYCLIC, 4096, 17669)  # 128 groups: two Toom-3 levels
     assert pl.t == 277 and pl.groups == 128 and pl.toom_levels == 2 and pl.toom_w == 16
     assert pl.N == 3 * pl.toom_M[0] >= 64 * 277
-    assert pl.leaf_words << pl.levels >= pl.toom_M[1] + 2 * pl.toom_w
+    assert pl.leaf_words << pl.levels >= pl.toom_M[1] + 2 * pl.toom_w_last
     assert pl.node_ctas == 128 * 25 * 3 ** pl.global_levels
     # one global level, folded into the resident-root interpolation
     assert pl.global_levels == 1 and pl.launches == 3 + 1 + 2 * 2 - 1
@@ -135,11 +135,27 @@ PLANNER_PINS = [
     (1, 256, 17669, 0), (1, 2048, 17669, 0), (1, 3072, 17669, 2), (1, 4096, 17669, 2),
     (1, 16384, 17669, 2), (1, 4096, 9000, 0), (1, 4096, 14000, 2), (1, 1024, 20000, 2),
     (1, 4096, 20000, 2), (1, 1024, 24000, 1), (1, 4096, 22000, 3), (1, 2048, 28000, 3),
-    (1, 4096, 28000, 3), (1, 4096, 30000, 2), (1, 32, 35851, 0), (1, 256, 35851, 0),
+    (1, 4096, 28000, 3), (1, 4096, 30000, 3), (1, 32, 35851, 0), (1, 256, 35851, 0),
     (1, 1024, 35851, 2), (1, 4096, 35851, 2), (1, 32, 57637, 0), (1, 256, 57637, 3),
     (1, 16384, 57637, 3), (0, 1 << 20, 64, 0), (0, 1 << 19, 128, 0), (0, 1 << 18, 256, 2),
     (0, 1 << 17, 512, 2), (0, 1 << 16, 1024, 2),
 ]
+
+
+def test_planner_innermost_point_pins(lib):
+    """The innermost Toom level evaluates at x = X^8 where that saves a leaf
+    word (measured: n=57637 x 16384 6583 -> 6402 us with LF 35 -> 34, n=30000
+    729 -> 631, n=32000 846 -> 763) and stays at X^16 elsewhere (d=32768:
+    25.4 vs 26.4 ms); never with the two-kernel interpolation of small levels."""
+    from paper_2201_10473_b200 import _lib
+
+    for kind, batch, size, wl, lf in ((1, 16384, 57637, 8, 34), (1, 4096, 30000, 8, 36), (1, 4096, 32000, 8, 28),
+                                      (1, 4096, 17669, 16, 32), (1, 4096, 35851, 16, 32), (0, 1 << 17, 512, 16, 29),
+                                      (0, 1 << 18, 256, 8, 29)):
+        pl = _lib.make_plan(kind, batch, size)
+        assert (pl.toom_w_last, pl.leaf_words) == (wl, lf), (kind, batch, size)
+        assert pl.leaf_words << pl.levels >= pl.toom_M[pl.toom_levels - 1] + 2 * pl.toom_w_last
+    assert _lib.make_plan(1, 2048, 17669).toom_w_last == 0  # no Toom level
 
 
 @pytest.mark.parametrize("kind,batch,size,tl", PLANNER_PINS)
@@ -378,7 +394,8 @@ def test_toom_plan_sizes(kind, size, tl):
     if p["toom_levels"]:
         Ms = p["toom_M"]
         assert 3 * Ms[0] >= 64 * t and len(Ms) == p["toom_levels"]
-        assert p["leaf_words"] << p["levels"] >= Ms[-1] + 2 * p["toom_w"]
+        assert p["toom_w_last"] in (8, p["toom_w"])
+        assert p["leaf_words"] << p["levels"] >= Ms[-1] + 2 * p["toom_w_last"]
 
 
 def test_row_chunks_bound_workspace(monkeypatch):
