@@ -360,7 +360,6 @@ struct ToomEvalGeo {
     int Tc;         // chunks per tile (Tc LF multiple of 4)
     int64_t G;      // groups
     int64_t Ns;     // storage words per node-problem operand
-    int wl;         // w of the innermost level's point x = X^wl (<= kToomW; windows keep the 2 kToomW halo)
 };
 
 constexpr int kEvalFusedThreads = 256;
@@ -471,12 +470,12 @@ __device__ __forceinline__ void eval_level5(const uint32_t *S, int Zs, uint32_t 
     }
 }
 
-template <int TL>
+template <int TL, int WL = kToomW>  // WL: the innermost level's point x = X^WL
 __global__ void __launch_bounds__(kEvalFusedThreads, 3)
 toom_eval_fused(const uint32_t *__restrict__ X0, uint32_t *__restrict__ Ya, uint32_t *__restrict__ Yb,
                 const ToomEvalGeo geo, int64_t x0_words) {
     constexpr int w = kToomW;
-    const int wl = geo.wl;  // the final level's point (its window still starts 2w before the tile)
+    constexpr int wl = WL;  // the final level's point (its window still starts 2w before the tile)
     constexpr int NP0 = efpow3(TL), Z0 = efslot(TL, 0);
     extern __shared__ __align__(16) uint32_t efs[];
     __shared__ __align__(8) uint64_t mbar;
@@ -1931,30 +1930,41 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
         geo.Tc = 8 * pl.leaf_words <= kEvalFusedMaxT ? 8 : 4;
         geo.G = G;
         geo.Ns = L.Ns;
-        geo.wl = L.wl;
         const int etiles = int(ceil_div(geo.chunks, geo.Tc));
         const size_t sm = size_t(eval_fused_smem_words(L.tl)) * 4;
         static std::atomic<uint32_t> ef_dev_mask{0};
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 31 && !(ef_dev_mask.load() & (1u << dev))) {
-            cudaError_t ae = cudaFuncSetAttribute(toom_eval_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  int(eval_fused_smem_words(1) * 4));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_eval_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(eval_fused_smem_words(2) * 4));
-            if (ae == cudaSuccess)
-                ae = cudaFuncSetAttribute(toom_eval_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(eval_fused_smem_words(3) * 4));
+            cudaError_t ae = cudaSuccess;
+#define F2X_EF_ATTR(TLV)                                                                                      \
+    if (ae == cudaSuccess)                                                                                    \
+        ae = cudaFuncSetAttribute(toom_eval_fused<TLV, kToomW>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                  int(eval_fused_smem_words(TLV) * 4));                                       \
+    if (ae == cudaSuccess)                                                                                    \
+        ae = cudaFuncSetAttribute(toom_eval_fused<TLV, kToomWSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  int(eval_fused_smem_words(TLV) * 4));
+            F2X_EF_ATTR(1)
+            F2X_EF_ATTR(2)
+            F2X_EF_ATTR(3)
+#undef F2X_EF_ATTR
             if (ae != cudaSuccess) return F2X_ECUDA - int(ae);
             ef_dev_mask.fetch_or(1u << dev);
         }
         const dim3 egrid(unsigned(etiles * G), 2);
         const int64_t x0w = 2 * G * int64_t(pl.N);
+#define F2X_EF_LAUNCH(TLV)                                                                                    \
+    do {                                                                                                      \
+        if (L.wl == kToomWSmall)                                                                              \
+            F2X_LAUNCH((toom_eval_fused<TLV, kToomWSmall>), egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, \
+                       x0w);                                                                                  \
+        else                                                                                                  \
+            F2X_LAUNCH((toom_eval_fused<TLV, kToomW>), egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); \
+    } while (0)
         switch (L.tl) {
-            case 1: F2X_LAUNCH(toom_eval_fused<1>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
-            case 2: F2X_LAUNCH(toom_eval_fused<2>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
-            default: F2X_LAUNCH(toom_eval_fused<3>, egrid, kEvalFusedThreads, sm, stream, X0a, Abs, Bbs, geo, x0w); break;
+            case 1: F2X_EF_LAUNCH(1); break;
+            case 2: F2X_EF_LAUNCH(2); break;
+            default: F2X_EF_LAUNCH(3); break;
         }
         if ((rc = debug_sync(stream, 2))) return rc;
     } else if (L.el == 0 && pl.N <= kTileCoeffs) {
