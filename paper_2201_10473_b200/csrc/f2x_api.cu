@@ -1542,9 +1542,16 @@ static bool k34_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int
     return k34_enabled() && TL == 0 && np > 0 && pass_levels[np - 1] <= 3 && G >= kK34MinGroups &&
            (ks + ks / 32) * 4 <= kK34SmemMax;
 }
-static bool kroot_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int64_t M_TL) {
-    return kroot_enabled() && TL > 0 && np > 0 && pass_levels[np - 1] == 1 &&
-           toom_use_seq(G * ipow5(TL - 1), M_TL) && int64_t(5) * kroot_hp(M_TL) * 4 <= kResSmemMax;
+// `root` = coefficients of the node problem (LF 2^K): its product (2 root
+// words, staged whole at slots k + 2w) must fit the resident span of
+// nb blk + 3w slots -- a node problem padded well past M + 2w does not
+// (n=54718: M = 2044, root 2112: 4224 > 4096 + 16), and keeps the separate pass.
+static bool kroot_fused(int TL, int np, const int32_t *pass_levels, int64_t G, int64_t M_TL, int64_t root) {
+    if (!(kroot_enabled() && TL > 0 && np > 0 && pass_levels[np - 1] == 1)) return false;
+    const int blk = toom_seq_blk(M_TL);
+    const int64_t nb = ceil_div(2 * M_TL, blk);
+    return toom_use_seq(G * ipow5(TL - 1), M_TL) && int64_t(5) * kroot_hp(M_TL) * 4 <= kResSmemMax &&
+           2 * root <= nb * blk + kToomWSmall;
 }
 
 // F2X_TOOM=0..3 forces the number of Toom-3 levels (tests / experiments)
@@ -1587,7 +1594,7 @@ static double karatsuba_pass_words(int kind, int t, int TL, int LF, int K, int64
         pass_levels[np++] = p;
         rem -= p;
     }
-    const bool folded = np > 0 && (kroot_fused(TL, np, pass_levels, G, M[TL]) ||
+    const bool folded = np > 0 && (kroot_fused(TL, np, pass_levels, G, M[TL], int64_t(LF) << K) ||
                                    k34_fused(TL, np, pass_levels, G, kind == F2X_KIND_FULL ? 2 * t : t));
     rem = GL;
     int64_t S = 2 * Ss;  // words of one product at the current level
@@ -1728,7 +1735,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
         rem -= p;
     }
     pl->num_passes = np;
-    pl->launches = 3 + np + 2 * TL - (kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ? 1 : 0) -
+    pl->launches = 3 + np + 2 * TL - (kroot_fused(TL, np, pl->pass_levels, G, bestM[TL], int64_t(LF) << K) ? 1 : 0) -
                    (k34_fused(TL, np, pl->pass_levels, G, kind == F2X_KIND_FULL ? 2 * t : t) ? 1 : 0);
     pl->cta_threads = e->threads;
     pl->node_ctas = G2 * ipow3(GL);
@@ -1773,7 +1780,7 @@ static int plan_impl(int kind, int64_t batch, int t_or_n, int leaf_hint, f2x_pla
     // interpolation or k34_root_unslice): it writes nothing to the ping-pong
     // buffers
     const int tout_pl = kind == F2X_KIND_FULL ? 2 * t : t;
-    const int np_exec = np - ((kroot_fused(TL, np, pl->pass_levels, G, bestM[TL]) ||
+    const int np_exec = np - ((kroot_fused(TL, np, pl->pass_levels, G, bestM[TL], int64_t(LF) << K) ||
                                k34_fused(TL, np, pl->pass_levels, G, tout_pl)) ? 1 : 0);
     int64_t p1 = 0;
     if (np_exec >= 1) {  // first pass output (the largest one written to P1)
@@ -2053,7 +2060,7 @@ static int run(int kind, const uint64_t *A, const uint64_t *B, uint64_t *C, int6
     int d = pl.global_levels;
     const int64_t in_stride0 = 2 * (L.Ns >> d);  // node products
     // last pass folded into the innermost Toom interpolation (resident roots)
-    const bool kroot = kroot_fused(L.tl, pl.num_passes, pl.pass_levels, G, L.M[L.tl]);
+    const bool kroot = kroot_fused(L.tl, pl.num_passes, pl.pass_levels, G, L.M[L.tl], int64_t(pl.leaf_words) << pl.levels);
     KRootIn kr{};
     const int tout = kind == F2X_KIND_FULL ? 2 * pl.t : pl.t;
     const bool k34 = k34_fused(L.tl, pl.num_passes, pl.pass_levels, G, tout);

@@ -282,3 +282,36 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", script, root, str(n), str(batch), str(tl)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
+def test_oversize_root_keeps_the_separate_pass(cuda):
+    """n=54718 on three Toom levels: M_3 = 2044 but the node problem is 33 * 64
+    = 2112 coefficients, so its 4224-word product does not fit the resident
+    span (2 x 2048 + 3w slots) of the resident-root interpolation -- found by
+    tools/stress_parity.py as an illegal shared-memory access.  The plan must
+    keep the separate k3_interp<1> pass there, and the product must match."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import c_mul_cyclic
+from oracle.f2x_oracle import make_cyclic_inputs
+from paper_2201_10473_b200 import mul_cyclic, plan
+n, batch = 54718, 942
+p = plan("cyclic", batch, n)
+assert p["toom_levels"] == 3 and p["leaf_words"] << p["levels"] == 2112 and p["toom_M"][-1] == 2044, p
+assert p["launches"] == 3 + p["num_passes"] + 2 * 3, p  # not folded
+A, B = make_cyclic_inputs(n, batch)
+d = lambda x: torch.from_numpy(x.view(np.int64)).cuda()
+got = mul_cyclic(d(A), d(B), n).cpu().numpy().view(np.uint64)
+rows = np.r_[0:16, batch - 16:batch]
+assert np.array_equal(got[rows], c_mul_cyclic(A[rows], B[rows], n))
+print("ok")
+"""
+    env = dict(os.environ, F2X_TOOM="3", F2X_TOOM_WLAST="16")
+    r = subprocess.run([sys.executable, "-c", script, root], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
