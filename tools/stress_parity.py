@@ -17,9 +17,24 @@ cases = int(sys.argv[1]) if len(sys.argv) > 1 else 120
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 dev = torch.device("cuda", 0)
 seen, bad = {}, 0
+K34 = os.environ.get("STRESS_K34") == "1"  # many-group Karatsuba-only shapes (k34_root_unslice, k1_slice_groups)
 for i in range(cases):
     cyc = i % 3 != 2
-    if cyc:
+    if K34:
+        batch = int(rng.integers(32768, 40000))
+        if cyc:
+            n = int(rng.integers(64, 9000))
+            p = plan("cyclic", batch, n)
+            A, B = make_cyclic_inputs(n, 4096)
+        else:
+            t = int(rng.integers(1, 139))
+            p = plan("full", batch, t)
+            A, B = make_full_inputs(t, 4096, words=True)
+        reps = -(-batch // 4096)
+        A, B = np.tile(A, (reps, 1))[:batch], np.tile(B, (reps, 1))[:batch]
+        dA, dB = torch.from_numpy(A.view(np.int64)).to(dev), torch.from_numpy(B.view(np.int64)).to(dev)
+        got = mul_cyclic(dA, dB, n) if cyc else mul_full(dA, dB)
+    elif cyc:
         n = int(rng.integers(10240, 70000))
         batch = int(rng.choice([rng.integers(1, 64), rng.integers(600, 1500), rng.integers(2000, 4200)]))
         p = plan("cyclic", batch, n)
