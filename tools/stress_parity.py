@@ -34,6 +34,13 @@ for i in range(cases):
         A, B = np.tile(A, (reps, 1))[:batch], np.tile(B, (reps, 1))[:batch]
         dA, dB = torch.from_numpy(A.view(np.int64)).to(dev), torch.from_numpy(B.view(np.int64)).to(dev)
         got = mul_cyclic(dA, dB, n) if cyc else mul_full(dA, dB)
+    elif os.environ.get("STRESS_BIG") == "1":  # very large operands at small batches (deep global Karatsuba levels)
+        cyc = False
+        t = int(rng.integers(1400, 9000))
+        batch = int(rng.choice([rng.integers(1, 8), rng.integers(8, 200)]))
+        p = plan("full", batch, t)
+        A, B = make_full_inputs(t, batch, words=True)
+        got = mul_full(torch.from_numpy(A.view(np.int64)).to(dev), torch.from_numpy(B.view(np.int64)).to(dev))
     elif cyc:
         n = int(rng.integers(10240, 70000))
         batch = int(rng.choice([rng.integers(1, 64), rng.integers(600, 1500), rng.integers(2000, 4200)]))
