@@ -120,7 +120,10 @@ print("ok", plan("cyclic", 40, 57637)["toom_levels"])
 
 
 @pytest.mark.parametrize("env", [{}, {"F2X_TOOM": "1"}, {"F2X_TOOM": "2", "F2X_TOOM_SEQ": "1"},
-                                 {"F2X_TOOM": "3", "F2X_TOOM_SEQ": "1"}, {"F2X_TOOM": "3"}])
+                                 {"F2X_TOOM": "3", "F2X_TOOM_SEQ": "1"}, {"F2X_TOOM": "3"},
+                                 # innermost level at x = X^8 (toom_eval_fused<TL, 8>, toom_interp_seq<.., 8>)
+                                 {"F2X_TOOM": "2", "F2X_TOOM_SEQ": "1", "F2X_TOOM_WLAST": "8"},
+                                 {"F2X_TOOM": "3", "F2X_TOOM_SEQ": "1", "F2X_TOOM_WLAST": "8"}])
 def test_checked_build_shared_memory_poison(env, cuda):
     from conftest import GOLDEN
     from paper_2201_10473_b200 import build as b
